@@ -1,0 +1,223 @@
+"""Pins of the oracle's FMM (oracle.c orc_fmm) and BFS against what the paper and the
+mathematics fix (trust order C.7):
+
+* FMM == brute-force value iteration (the literal definition, C.1) on tiny random grids with
+  F = 0 obstacles, enclosed pockets and random exits (q >= 0)           -- S:190
+* reachability mask == BFS (exact graph property, R11)
+* F = 1 point source: the 6 half-axes are exactly d*h (north_star pin, R2)
+* F = 1 point source: U = W(|i-c|,|j-c|,|k-c|) h, W the corner-source table from value
+  iteration (octant = corner solve, h = 2^-k scaling exact)
+* plane wave with non-uniform F(k): U = cumulative sum of h/F_k exactly (C4's slab pin)
+* F -> 2F, q -> q/2 gives U -> U/2 bit-exact; adding exits never raises U (comparison)
+* symmetry (48 maps) of the F = 1 centre source
+* C3 sibling: the exit block's discrete ball equals the F = 1 solution bit-exact; comparison
+  bounds W h / 10 <= U <= W h
+* invariants on every output: Eq. (2) residual, Lipschitz, causal parent, monotone pops
+* first-order convergence to |x - x0| for F = 1 (sanity)
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+
+def _run_both(w):
+    U = oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals)
+    V = oracle.value_iteration(w.n, w.F, w.exit_mask, w.exit_vals)
+    return U, V
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fmm_equals_value_iteration_random(seed):
+    n = [4, 6, 8, 11, 12, 16][seed % 6]
+    w = W.random_instance(n, seed, p_wall=0.2, n_exits=1 + seed % 4,
+                          q_max=(0.3 if seed % 3 == 0 else 0.0))
+    U, V = _run_both(w)
+    fin = np.isfinite(V)
+    assert np.array_equal(np.isfinite(U), fin)
+    assert np.abs(U[fin] - V[fin]).max() <= 1e-13
+    R = oracle.bfs(n, w.F, w.exit_mask)
+    assert np.array_equal(R.astype(bool), fin)
+    # exits exactly q
+    ex = w.exit_mask.astype(bool)
+    assert np.array_equal(U[ex], w.exit_vals[ex])
+
+
+def test_enclosed_pocket_and_f0_exit():
+    n = 12
+    F = np.ones((n + 1,) * 3)
+    # a closed box shell of F = 0 around an interior pocket
+    F[3:9, 3:9, 3:9] = 0.0
+    F[4:8, 4:8, 4:8] = 1.0
+    mask = np.zeros(F.shape, np.uint8)
+    q = np.zeros(F.shape)
+    mask[0, 0, 0] = 1
+    mask[12, 12, 12] = 1
+    F[12, 12, 12] = 0.0           # an exit with F = 0 keeps q (R11)
+    q[12, 12, 12] = 0.25
+    U = oracle.fmm(n, F, mask, q)
+    V = oracle.value_iteration(n, F, mask, q)
+    assert np.isinf(U[4:8, 4:8, 4:8]).all()
+    assert np.isinf(U[F == 0][~mask[F == 0].astype(bool)]).all()
+    assert U[12, 12, 12] == 0.25
+    fin = np.isfinite(V)
+    assert np.array_equal(np.isfinite(U), fin)
+    assert np.abs(U[fin] - V[fin]).max() <= 1e-13
+    assert np.array_equal(oracle.bfs(n, F, mask).astype(bool), fin)
+
+
+def _corner_table(m):
+    """W on [0..m]^3: F = 1 corner source at (0,0,0), value iteration, units of h (h = 1)."""
+    w = W.Workload("corner", m, np.ones((m + 1,) * 3), np.zeros((m + 1,) * 3, np.uint8),
+                   np.zeros((m + 1,) * 3))
+    w.exit_mask[0, 0, 0] = 1
+    return oracle.value_iteration(m, w.F, w.exit_mask, w.exit_vals, h=1.0)
+
+
+@pytest.fixture(scope="module")
+def corner64():
+    return _corner_table(64)
+
+
+def test_corner_table_closed_forms(corner64):
+    Wt = corner64  # [k, j, i]
+    s2, s3 = 1 / math.sqrt(2), 1 / math.sqrt(3)
+    assert Wt[0, 0, 1] == 1.0
+    assert Wt[0, 1, 1] == pytest.approx(1 + s2, rel=1e-15)
+    assert Wt[1, 1, 1] == pytest.approx(1 + s2 + s3, rel=1e-15)
+    for d in range(65):  # axes exactly d (R2)
+        assert Wt[0, 0, d] == d and Wt[0, d, 0] == d and Wt[d, 0, 0] == d
+    # truncation independence: a smaller box gives the same values (causality)
+    W32 = _corner_table(32)
+    assert np.array_equal(W32, Wt[:33, :33, :33])
+
+
+@pytest.mark.parametrize("n", [16, 32, 64, 128])
+def test_c1_point_source_equals_corner_table(n, corner64):
+    w = W.c1(n)
+    U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+    c = n // 2
+    h = 1.0 / n
+    idx = np.abs(np.arange(n + 1) - c)
+    expect = corner64[idx][:, idx][:, :, idx] * h
+    assert np.array_equal(U, expect)
+    # half axes exactly d*h
+    for d in range(c + 1):
+        for (a, b, e) in ((c + d, c, c), (c - d, c, c), (c, c + d, c), (c, c - d, c),
+                          (c, c, c + d), (c, c, c - d)):
+            assert U[e, b, a] == d * h
+
+
+def test_symmetry_48(corner64):
+    n = 32
+    w = W.c1(n)
+    U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+    for perm in itertools.permutations(range(3)):
+        for flips in itertools.product([False, True], repeat=3):
+            V = np.transpose(U, perm)
+            for ax, f in enumerate(flips):
+                if f:
+                    V = np.flip(V, ax)
+            assert np.array_equal(U, V)
+
+
+def test_plane_wave_cumsum_exact():
+    n = 24
+    rng = np.random.default_rng(3)
+    Fk = rng.uniform(0.3, 3.0, n + 1)
+    F = np.broadcast_to(Fk[:, None, None], (n + 1,) * 3).copy()
+    mask = np.zeros(F.shape, np.uint8)
+    mask[0] = 1
+    q = np.zeros(F.shape)
+    U = oracle.fmm(n, F, mask, q)
+    h = 1.0 / n
+    expect = np.concatenate([[0.0], np.cumsum(h / Fk[1:])])
+    assert np.array_equal(U, np.broadcast_to(expect[:, None, None], U.shape))
+
+
+def test_scaling_and_added_exits():
+    w = W.random_instance(12, 77, p_wall=0.1, n_exits=3, q_max=0.4)
+    U = oracle.fmm(12, w.F, w.exit_mask, w.exit_vals)
+    U2 = oracle.fmm(12, 2 * w.F, w.exit_mask, w.exit_vals / 2)
+    assert np.array_equal(U2, U / 2)
+    m2 = w.exit_mask.copy()
+    m2[5, 5, 5] = 1
+    q2 = w.exit_vals.copy()
+    q2[5, 5, 5] = 0.0
+    U3 = oracle.fmm(12, w.F, m2, q2)
+    assert (U3 <= U).all()
+
+
+def test_c3_sibling_ball_and_bounds(corner64):
+    n = 64  # 8-point blocks; the exit block (F = 1) is [0, 8)^3
+    w = W.c3(n)
+    U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+    h = 1.0 / n
+    Wh = corner64 * h
+    ball = Wh < 7 * h
+    assert np.array_equal(U[ball], Wh[ball])
+    # edge U(i, 0, 0) = i h inside the first block
+    for i in range(8):
+        assert U[0, 0, i] == i * h
+    # comparison principle: F in [1, 10] => W h / 10 <= U <= W h
+    assert (U <= Wh * (1 + 1e-12)).all()
+    assert (U >= Wh / 10 * (1 - 1e-12)).all()
+    assert not np.array_equal(U, Wh)  # the fast blocks do matter
+
+
+def test_c2_sibling_bounds_and_symmetry():
+    n = 64
+    w = W.c2(n)
+    U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+    Wc = oracle.fmm(n, np.ones_like(w.F), w.exit_mask, w.exit_vals)  # F = 1 about the exit
+    assert (U <= Wc * 2 * (1 + 1e-12)).all() and (U >= Wc * (2 / 3) * (1 - 1e-12)).all()
+    # F is symmetric under axis permutations and pairs of reflections about the centre
+    for perm in itertools.permutations(range(3)):
+        assert np.abs(np.transpose(U, perm) - U).max() < 1e-12
+    V = np.flip(np.flip(U, 0), 1)
+    assert np.abs(V - U).max() < 1e-12
+
+
+def test_c4_sibling_slab_plane_wave_and_mask():
+    n = 64
+    w = W.c4(n)
+    U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+    h = 1.0 / n
+    k0 = w.meta["walls"][0]
+    kk = np.arange(n + 1)[:, None, None] * h
+    open_ = w.F > 0
+    slab = (np.arange(n + 1) <= k0)[:, None, None] & open_
+    assert np.array_equal(U[slab], np.broadcast_to(kk, U.shape)[slab])
+    fin = np.isfinite(U)
+    assert (U[fin] >= np.broadcast_to(kk, U.shape)[fin]).all()  # F <= 1 comparison
+    assert np.array_equal(oracle.bfs(n, w.F, w.exit_mask).astype(bool), fin)
+    assert np.isinf(U[~open_]).all()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_invariants_on_siblings(name):
+    n = 32
+    w = W.make(name, n)
+    U, cnt = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals, return_count=True)
+    st = oracle.check(n, w.F, w.exit_mask, U)
+    assert st["res_max"] < 1e-12
+    assert st["lip_max"] <= 1e-12  # a few ulp(U)/hf
+    assert st["causal_bad"] == 0 and st["f0_finite"] == 0 and st["inf_bad"] == 0
+    R = oracle.bfs(n, w.F, w.exit_mask)
+    assert cnt == int(R.sum())  # each reachable point accepted exactly once
+
+
+def test_first_order_convergence():
+    errs = []
+    for n in (16, 32, 64):
+        w = W.c1(n)
+        U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+        x = np.arange(n + 1) / n - 0.5
+        d = np.sqrt(x[:, None, None] ** 2 + x[None, :, None] ** 2 + x[None, None, :] ** 2)
+        errs.append(np.abs(U - d).max())
+    assert errs[0] / errs[1] >= 1.0 and errs[1] / errs[2] >= 1.0
+    assert errs[2] < errs[0]

@@ -1,0 +1,131 @@
+/*
+ * eik.h -- C ABI of the B200-native cell-sweep Eikonal solver (pHCM hot path, arXiv 1306.4743).
+ *
+ * Problem exported (Eq. (1)-(2)):
+ *   |grad u| F = 1 on the (n+1)^3 uniform grid of [0, n h]^3, u = q on the exit set Q'
+ *   (exits may be anywhere; reading R8), values outside the cube are +inf,
+ *   discretised by the first-order upwind scheme of Eq. (2) and solved to the
+ *   discrete fixed point (kappa = 0; reading R13) by cell-level Gauss-Seidel
+ *   processing (HCM, Alg. 1-2) scheduled on the GPU (pHCM Alg. 3 analogue).
+ *
+ * Layout of every array argument: contiguous, lexicographic with i fastest,
+ *   idx = i + (n+1)*(j + (n+1)*k),  M = (n+1)^3
+ * dtype: float (EIK_F32) or double (EIK_F64) for F, exit_vals and U_out; uint8 for exit_mask.
+ *
+ * Ownership: the caller owns F, exit_mask, exit_vals, U_out (valid until the call returns).
+ * The ctx owns its scratch (padded cell tiles, keys, flags, worklists), grown lazily, reused
+ * across solves, freed by eik_destroy.  One ctx per host thread; no internal locking.
+ *
+ * Errors: every call returns an eik_status; text via eik_last_error.  Nothing throws or aborts
+ * across the ABI.  On EIK_EINVAL U_out is untouched.
+ */
+#ifndef EIK_H_
+#define EIK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIK_ABI_VERSION 1
+
+typedef struct eik_ctx eik_ctx;
+
+typedef enum {
+    EIK_OK = 0,
+    EIK_EINVAL = 1,     /* bad argument or input data (see eik_solve); U_out untouched      */
+    EIK_ENOMEM = 2,     /* device scratch allocation failed                                  */
+    EIK_ECUDA = 3,      /* a CUDA runtime error (message carries cudaGetErrorString)          */
+    EIK_ENOTSUP = 4,    /* device is not compute capability 10.x (sm_100a build)              */
+    EIK_EINTERNAL = 5   /* internal limit hit (e.g. max rounds) -- a bug or a debug knob      */
+} eik_status;
+
+typedef enum { EIK_F32 = 0, EIK_F64 = 1 } eik_precision;
+
+/* Options for eik_set_option (all optional; defaults in brackets). */
+typedef enum {
+    EIK_OPT_BIN_WIDTH = 0,   /* Delta of the priority bins, in units of time (same units as U).
+                                Cells whose key lies in [kmin, kmin + Delta] are processed in a
+                                round ("cells in the lowest range of values").  <= 0 or
+                                +inf = every queued cell each round.  [+inf]                    */
+    EIK_OPT_MAX_ROUNDS = 1,  /* safety cap on scheduler rounds; exceeding it = EIK_EINTERNAL
+                                [1e9]                                                           */
+    EIK_OPT_LOOP_MODE = 2,   /* 0 = device-resident loop (CUDA graph WHILE node, no host
+                                round-trip per round); 1 = host-driven loop (debug) [0]          */
+    EIK_OPT_COLLECT_STATS = 3 /* 1 = count point updates/writes/sweeps on device [1]            */
+} eik_option;
+
+/* Work and time counters of the last successful solve. */
+typedef struct {
+    int64_t  M;                 /* (n+1)^3 real gridpoints                                   */
+    int64_t  padded_points;     /* (cps*r)^3 stored points                                   */
+    int64_t  J;                 /* cells, cps^3                                              */
+    int32_t  cells_per_side;    /* cps = ceil((n+1)/r)                                       */
+    int32_t  cell_size;         /* r                                                         */
+    int32_t  precision;         /* eik_precision                                             */
+    int32_t  pad_;
+    uint64_t point_updates;     /* local solves executed (Alg. 2 line 5)                     */
+    uint64_t point_writes;      /* strict decreases (Alg. 2 line 7)                          */
+    uint64_t cell_processings;  /* heap-removal analogue (Alg. 1 line 4)                     */
+    uint64_t cell_sweeps;       /* sweeps over all processings (AvS numerator)       */
+    uint64_t real_points_processed; /* sum over processings of real points in the cell      */
+    uint32_t rounds;            /* scheduler rounds (select -> process -> re-activate)       */
+    uint32_t max_worklist;      /* largest number of cells processed in one round            */
+    uint64_t bytes_min;         /* north-star minimum bytes: P_eq * M * (sF + sU), D.4       */
+    uint64_t bytes_cell_alg;    /* algorithmic cell-sweep bytes: per processing
+                                   (2 r^3 + 6 r^2) s read + (changed points) s written          */
+    double   ms_ingest, ms_loop, ms_egress, ms_total;   /* CUDA events on the ctx stream      */
+} eik_stats;
+
+/* Create a context on `device`.  cuda_stream: a cudaStream_t to enqueue on (e.g. torch's
+ * current stream), or NULL to let the ctx create and own a non-blocking stream.
+ * Returns EIK_ENOTSUP if the device is not sm_100. */
+int eik_create(eik_ctx** out, int device, void* cuda_stream);
+
+/* Change the stream subsequent solves enqueue on (NULL = the ctx's own stream). */
+int eik_set_stream(eik_ctx* ctx, void* cuda_stream);
+
+/* Set an eik_option.  EIK_EINVAL for an unknown option or a bad value. */
+int eik_set_option(eik_ctx* ctx, int option, double value);
+
+/* Solve with DEVICE pointers (CUDA device memory, e.g. torch CUDA tensors).
+ *   n          >= 1 intervals per side (n+1 points per side)
+ *   h          > 0, finite grid spacing (the problem's 1/n for [0,1]^3)
+ *   F          M x dtype speeds; finite, >= 0; 0 = impassable (reading R11)
+ *   exit_mask  M x uint8; nonzero = exit gridpoint; at least one exit (R10)
+ *   exit_vals  M x dtype; q, read where exit_mask != 0; finite, >= 0 (R9; -0 -> +0)
+ *   U_out      M x dtype; written only on EIK_OK: q at exits, the discrete solution at
+ *              reachable points, +inf at unreachable ones (F = 0 walls, enclosed pockets)
+ *   precision  EIK_F32 (storage and arithmetic in fp32, R14) or EIK_F64
+ *   cell_size  r in {4, 8, 16} gridpoints per cell side; (n+1) need not be a
+ *              multiple of r: cells are padded with never-updated "outside" points (R12)
+ * Blocking: returns after the work on the ctx stream completes, so the status (including
+ * device-detected input errors) is final.
+ * EIK_EINVAL: null ctx/pointer, n < 1, h <= 0 or non-finite, bad precision or cell_size,
+ * any F < 0 / NaN / inf, any exit q < 0 / NaN / inf, or no exit point. */
+int eik_solve(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
+              const void* exit_vals, void* U_out, int precision, int cell_size);
+
+/* Same contract with HOST pointers (pageable or pinned).  The host->device copies of the
+ * inputs and the device->host copy of U happen inside the call (the e2e path). */
+int eik_solve_host(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
+                   const void* exit_vals, void* U_out, int precision, int cell_size);
+
+/* Stats of the last successful solve.  EIK_EINVAL if ctx/out is NULL. */
+int eik_get_stats(const eik_ctx* ctx, eik_stats* out);
+
+/* Message of the last failing call on ctx (owned by ctx; valid until its next call).
+ * eik_last_error(NULL) returns the message of the last failed eik_create. */
+const char* eik_last_error(const eik_ctx* ctx);
+
+/* Free scratch (and the ctx's own stream). NULL-safe. */
+void eik_destroy(eik_ctx* ctx);
+
+/* EIK_ABI_VERSION of the loaded library. */
+int eik_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EIK_H_ */

@@ -1,0 +1,190 @@
+"""B200-native cell-sweep Eikonal solver (hot path of the parallel Heap-Cell Method,
+Chacon & Vladimirsky, arXiv 1306.4743).
+
+Thin Python binding over the C ABI in include/eik.h (libeik.so, built in-tree for sm_100a).
+Argument marshalling only: every step of the solve runs in the CUDA kernels of
+csrc/eik_kernels.cuh.  PyTorch provides device memory and the current stream.  There is no
+CPU fallback: if libeik.so is missing or cannot be loaded, importing this package raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libeik.so")
+
+EIK_OK, EIK_EINVAL, EIK_ENOMEM, EIK_ECUDA, EIK_ENOTSUP, EIK_EINTERNAL = range(6)
+EIK_F32, EIK_F64 = 0, 1
+EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS = range(4)
+STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
+                4: "EIK_ENOTSUP", 5: "EIK_EINTERNAL"}
+
+# every symbol include/eik.h declares (checked by tests/test_abi.py)
+EXPORTS = ("eik_create", "eik_set_stream", "eik_set_option", "eik_solve", "eik_solve_host",
+           "eik_get_stats", "eik_last_error", "eik_destroy", "eik_abi_version")
+
+
+class EikStats(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int64), ("padded_points", ctypes.c_int64), ("J", ctypes.c_int64),
+                ("cells_per_side", ctypes.c_int32), ("cell_size", ctypes.c_int32),
+                ("precision", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("point_updates", ctypes.c_uint64), ("point_writes", ctypes.c_uint64),
+                ("cell_processings", ctypes.c_uint64), ("cell_sweeps", ctypes.c_uint64),
+                ("real_points_processed", ctypes.c_uint64),
+                ("rounds", ctypes.c_uint32), ("max_worklist", ctypes.c_uint32),
+                ("bytes_min", ctypes.c_uint64), ("bytes_cell_alg", ctypes.c_uint64),
+                ("ms_ingest", ctypes.c_double), ("ms_loop", ctypes.c_double),
+                ("ms_egress", ctypes.c_double), ("ms_total", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+class EikError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, I64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+    lib.eik_create.argtypes = [ctypes.POINTER(P), I, P]
+    lib.eik_create.restype = I
+    lib.eik_set_stream.argtypes = [P, P]
+    lib.eik_set_stream.restype = I
+    lib.eik_set_option.argtypes = [P, I, D]
+    lib.eik_set_option.restype = I
+    for f in (lib.eik_solve, lib.eik_solve_host):
+        f.argtypes = [P, I64, D, P, P, P, P, I, I]
+        f.restype = I
+    lib.eik_get_stats.argtypes = [P, ctypes.POINTER(EikStats)]
+    lib.eik_get_stats.restype = I
+    lib.eik_last_error.argtypes = [P]
+    lib.eik_last_error.restype = ctypes.c_char_p
+    lib.eik_destroy.argtypes = [P]
+    lib.eik_destroy.restype = None
+    lib.eik_abi_version.argtypes = []
+    lib.eik_abi_version.restype = I
+    return lib
+
+
+lib = _load()
+
+
+def _n_from_numel(numel: int) -> int:
+    n1 = round(numel ** (1.0 / 3.0))
+    for c in (n1 - 1, n1, n1 + 1):
+        if c > 0 and c ** 3 == numel:
+            return c - 1
+    raise ValueError(f"array of {numel} elements is not an (n+1)^3 grid")
+
+
+class Solver:
+    """One eik_ctx (device scratch reused across solves)."""
+
+    def __init__(self, device: int = 0, stream=None, bin_width: float | None = None,
+                 loop_mode: int = 0, collect_stats: bool = True):
+        self._ctx = ctypes.c_void_p()
+        st = lib.eik_create(ctypes.byref(self._ctx), device, stream)
+        if st != EIK_OK:
+            raise EikError(st, lib.eik_last_error(None).decode())
+        self.device = device
+        if bin_width is not None:
+            self.set_option(EIK_OPT_BIN_WIDTH, bin_width)
+        if loop_mode:
+            self.set_option(EIK_OPT_LOOP_MODE, loop_mode)
+        if not collect_stats:
+            self.set_option(EIK_OPT_COLLECT_STATS, 0)
+
+    def _err(self, st):
+        return EikError(st, lib.eik_last_error(self._ctx).decode())
+
+    def set_option(self, opt: int, value: float):
+        st = lib.eik_set_option(self._ctx, opt, float(value))
+        if st != EIK_OK:
+            raise self._err(st)
+
+    def close(self):
+        if self._ctx:
+            lib.eik_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device tensors ------------------------------------------------------------------
+    def solve(self, F, exit_mask, exit_vals, h: float | None = None, cell_size: int = 16,
+              n: int | None = None, out=None):
+        """F, exit_mask (uint8), exit_vals: contiguous CUDA tensors of (n+1)^3 elements,
+        lexicographic i fastest.  dtype of F (float32/float64) selects the precision.
+        Returns U (same shape/dtype as F).  Enqueued on torch's current stream; blocking."""
+        import torch
+        if F.dtype not in (torch.float32, torch.float64):
+            raise TypeError("F must be float32 or float64")
+        prec = EIK_F32 if F.dtype == torch.float32 else EIK_F64
+        for t in (F, exit_mask, exit_vals):
+            if not (t.is_cuda and t.is_contiguous()):
+                raise ValueError("solve() takes contiguous CUDA tensors (use solve_host for host arrays)")
+        if exit_mask.dtype != torch.uint8 or exit_vals.dtype != F.dtype:
+            raise TypeError("exit_mask must be uint8 and exit_vals must have F's dtype")
+        n = _n_from_numel(F.numel()) if n is None else n
+        h = 1.0 / n if h is None else h
+        if out is None:
+            out = torch.empty_like(F)
+        stream = torch.cuda.current_stream(F.device).cuda_stream
+        lib.eik_set_stream(self._ctx, ctypes.c_void_p(stream))
+        st = lib.eik_solve(self._ctx, n, h, F.data_ptr(), exit_mask.data_ptr(),
+                           exit_vals.data_ptr(), out.data_ptr(), prec, cell_size)
+        if st != EIK_OK:
+            raise self._err(st)
+        return out
+
+    # -- host arrays (e2e path: H2D + solve + D2H inside the C call) ---------------------
+    def solve_host(self, F, exit_mask, exit_vals, h: float | None = None, cell_size: int = 16,
+                   n: int | None = None, out=None):
+        """numpy arrays (or pinned CPU torch tensors) in host memory."""
+        import numpy as np
+
+        def ptr(a):
+            return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
+
+        dt = F.dtype
+        is_f32 = (dt == np.float32) if isinstance(F, np.ndarray) else (str(dt) == "torch.float32")
+        prec = EIK_F32 if is_f32 else EIK_F64
+        numel = F.size if isinstance(F, np.ndarray) else F.numel()
+        n = _n_from_numel(numel) if n is None else n
+        h = 1.0 / n if h is None else h
+        if out is None:
+            out = np.empty_like(F) if isinstance(F, np.ndarray) else F.new_empty(F.shape)
+        lib.eik_set_stream(self._ctx, None)
+        st = lib.eik_solve_host(self._ctx, n, h, ptr(F), ptr(exit_mask), ptr(exit_vals),
+                                ptr(out), prec, cell_size)
+        if st != EIK_OK:
+            raise self._err(st)
+        return out
+
+    def stats(self) -> dict:
+        s = EikStats()
+        st = lib.eik_get_stats(self._ctx, ctypes.byref(s))
+        if st != EIK_OK:
+            raise self._err(st)
+        return s.as_dict()
+
+
+_default: Solver | None = None
+
+
+def solve(F, exit_mask, exit_vals, h: float | None = None, cell_size: int = 16, out=None):
+    """Module-level convenience: solve on a shared per-process Solver (device of F)."""
+    global _default
+    if _default is None:
+        _default = Solver(device=F.device.index or 0)
+    return _default.solve(F, exit_mask, exit_vals, h=h, cell_size=cell_size, out=out)

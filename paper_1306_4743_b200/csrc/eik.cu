@@ -1,0 +1,515 @@
+// eik.cu -- host driver and C ABI (include/eik.h) of the B200 cell-sweep Eikonal solver.
+//
+// PRODUCT PATH: validate -> size/alloc scratch -> enqueue the device phases on the ctx stream
+// -> one small D2H of the control block -> return status.  The scheduler loop runs on the
+// device (CUDA graph with a conditional WHILE node: no host round-trip per round); a
+// host-driven loop is kept as a debug mode (EIK_OPT_LOOP_MODE = 1).  No CPU fallback.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/eik.h"
+#include "eik_kernels.cuh"
+
+using namespace eik;
+
+struct eik_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    // options
+    double bin_width = INFINITY;
+    uint32_t max_rounds = 1000000000u;
+    int loop_mode = 0;
+    int collect_stats = 1;
+    // scratch
+    void* Vt = nullptr;
+    void* Ht = nullptr;
+    size_t tile_bytes = 0;        // capacity of Vt / Ht each
+    uint32_t* key = nullptr;
+    uint32_t* state = nullptr;
+    uint32_t* wl0 = nullptr;
+    uint32_t* wl1 = nullptr;
+    uint32_t* proc_cell = nullptr;
+    uint32_t* proc_flags = nullptr;
+    size_t cell_cap = 0;
+    Ctl* ctl = nullptr;
+    Ctl* ctl_host = nullptr;      // pinned
+    // plane tables per r (index 0: r=4, 1: r=8, 2: r=16)
+    uint16_t* plane_tab[3] = {nullptr, nullptr, nullptr};
+    int32_t* plane_off[3] = {nullptr, nullptr, nullptr};
+    // host-pointer staging (eik_solve_host)
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
+    // graph cache
+    cudaGraphExec_t gexec = nullptr;
+    std::string gkey;
+    // events
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    eik_stats stats{};
+    bool have_stats = false;
+};
+
+static std::string g_create_err;
+
+static int fail(eik_ctx* ctx, int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    else g_create_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            (void)cudaGetLastError();                                                      \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? EIK_ENOMEM : EIK_ECUDA,     \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+        }                                                                                  \
+    } while (0)
+
+static int rindex_of(int r) { return r == 4 ? 0 : r == 8 ? 1 : r == 16 ? 2 : -1; }
+
+// wavefront plane table for an r^3 cell: entries (a | b<<4 | c<<8) sorted by plane a+b+c
+static void make_plane_table(int r, std::vector<uint16_t>& tab, std::vector<int32_t>& off)
+{
+    const int npl = 3 * r - 2;
+    tab.clear();
+    off.assign(npl + 1, 0);
+    for (int s = 0; s < npl; ++s) {
+        off[s] = (int32_t)tab.size();
+        for (int c = 0; c < r; ++c)
+            for (int b = 0; b < r; ++b) {
+                const int a = s - b - c;
+                if (a >= 0 && a < r) tab.push_back((uint16_t)(a | (b << 4) | (c << 8)));
+            }
+    }
+    off[npl] = (int32_t)tab.size();
+}
+
+extern "C" int eik_abi_version(void) { return EIK_ABI_VERSION; }
+
+extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
+{
+    eik_ctx* ctx = nullptr;
+    if (!out) return fail(nullptr, EIK_EINVAL, "eik_create: out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, EIK_ECUDA, "eik_create: no CUDA device (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev)
+        return fail(nullptr, EIK_EINVAL, "eik_create: device %d out of range [0,%d)", device, ndev);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+        return fail(nullptr, EIK_ECUDA, "eik_create: cudaGetDeviceProperties failed");
+    if (prop.major != 10)
+        return fail(nullptr, EIK_ENOTSUP, "eik_create: device %d is sm_%d%d; this build is sm_100a only",
+                    device, prop.major, prop.minor);
+    ctx = new eik_ctx();
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    CK(cudaSetDevice(device));
+    if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
+    else {
+        CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream;
+    }
+    CK(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
+    CK(cudaMallocHost(&ctx->ctl_host, sizeof(Ctl)));
+    for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&ctx->ev[i]));
+    const int rs[3] = {4, 8, 16};
+    for (int t = 0; t < 3; ++t) {
+        std::vector<uint16_t> tab;
+        std::vector<int32_t> off;
+        make_plane_table(rs[t], tab, off);
+        CK(cudaMalloc(&ctx->plane_tab[t], tab.size() * sizeof(uint16_t)));
+        CK(cudaMalloc(&ctx->plane_off[t], off.size() * sizeof(int32_t)));
+        CK(cudaMemcpy(ctx->plane_tab[t], tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->plane_off[t], off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    // opt in to > 48 KB dynamic shared memory for the cell kernels
+    CK(cudaFuncSetAttribute(k_cell<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
+    CK(cudaFuncSetAttribute(k_cell<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 16>()));
+    CK(cudaFuncSetAttribute(k_cell<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 8>()));
+    CK(cudaFuncSetAttribute(k_cell<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 8>()));
+    CK(cudaFuncSetAttribute(k_cell<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 4>()));
+    CK(cudaFuncSetAttribute(k_cell<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 4>()));
+    *out = ctx;
+    return EIK_OK;
+}
+
+static void free_scratch(eik_ctx* ctx)
+{
+    cudaFree(ctx->Vt); cudaFree(ctx->Ht);
+    cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
+    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags);
+    ctx->Vt = ctx->Ht = nullptr;
+    ctx->key = ctx->state = ctx->wl0 = ctx->wl1 = ctx->proc_cell = ctx->proc_flags = nullptr;
+    ctx->tile_bytes = ctx->cell_cap = 0;
+}
+
+extern "C" void eik_destroy(eik_ctx* ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    free_scratch(ctx);
+    cudaFree(ctx->stage);
+    cudaFree(ctx->ctl);
+    cudaFreeHost(ctx->ctl_host);
+    for (int t = 0; t < 3; ++t) { cudaFree(ctx->plane_tab[t]); cudaFree(ctx->plane_off[t]); }
+    for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    (void)cudaGetLastError();
+    delete ctx;
+}
+
+extern "C" int eik_set_stream(eik_ctx* ctx, void* cuda_stream)
+{
+    if (!ctx) return EIK_EINVAL;
+    cudaStream_t s = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own_stream;
+    if (!s) {
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+        s = ctx->own_stream;
+    }
+    ctx->stream = s;
+    return EIK_OK;
+}
+
+extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
+{
+    if (!ctx) return EIK_EINVAL;
+    switch (option) {
+    case EIK_OPT_BIN_WIDTH:
+        if (isnan(value)) return fail(ctx, EIK_EINVAL, "bin width is NaN");
+        ctx->bin_width = value <= 0 ? INFINITY : value;
+        return EIK_OK;
+    case EIK_OPT_MAX_ROUNDS:
+        if (!(value >= 1)) return fail(ctx, EIK_EINVAL, "max rounds must be >= 1");
+        ctx->max_rounds = value > 4e9 ? 0xffffffffu : (uint32_t)value;
+        return EIK_OK;
+    case EIK_OPT_LOOP_MODE:
+        if (value != 0 && value != 1) return fail(ctx, EIK_EINVAL, "loop mode must be 0 or 1");
+        ctx->loop_mode = (int)value;
+        return EIK_OK;
+    case EIK_OPT_COLLECT_STATS:
+        ctx->collect_stats = value != 0;
+        return EIK_OK;
+    default:
+        return fail(ctx, EIK_EINVAL, "unknown option %d", option);
+    }
+}
+
+extern "C" int eik_get_stats(const eik_ctx* ctx, eik_stats* out)
+{
+    if (!ctx || !out) return EIK_EINVAL;
+    if (!ctx->have_stats) {
+        memset(out, 0, sizeof *out);
+        return EIK_EINVAL;
+    }
+    *out = ctx->stats;
+    return EIK_OK;
+}
+
+extern "C" const char* eik_last_error(const eik_ctx* ctx)
+{
+    return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+// ---------------------------------------------------------------------------------------
+static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
+{
+    if (tile_bytes > ctx->tile_bytes || J > ctx->cell_cap) {
+        if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+        CK(cudaStreamSynchronize(ctx->stream));
+        free_scratch(ctx);
+        CK(cudaMalloc(&ctx->Vt, tile_bytes));
+        CK(cudaMalloc(&ctx->Ht, tile_bytes));
+        ctx->tile_bytes = tile_bytes;
+        CK(cudaMalloc(&ctx->key, J * 4));
+        CK(cudaMalloc(&ctx->state, J * 4));
+        CK(cudaMalloc(&ctx->wl0, J * 4));
+        CK(cudaMalloc(&ctx->wl1, J * 4));
+        CK(cudaMalloc(&ctx->proc_cell, J * 4));
+        CK(cudaMalloc(&ctx->proc_flags, J * 4));
+        ctx->cell_cap = J;
+    }
+    return EIK_OK;
+}
+
+template <typename T, int R>
+static int launch_cell(eik_ctx* ctx, const CellArgs& a, int grid)
+{
+    k_cell<T, R><<<grid, CellCfg<R>::NT, cell_smem_bytes<T, R>(), ctx->stream>>>(a);
+    CK(cudaGetLastError());
+    return EIK_OK;
+}
+
+template <typename T>
+static int cell_grid(eik_ctx* ctx, int r, int* grid)
+{
+    int occ = 0;
+    cudaError_t e;
+    if (r == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cell<T, 16>, CellCfg<16>::NT, cell_smem_bytes<T, 16>());
+    else if (r == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cell<T, 8>, CellCfg<8>::NT, cell_smem_bytes<T, 8>());
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cell<T, 4>, CellCfg<4>::NT, cell_smem_bytes<T, 4>());
+    CK(e);
+    if (occ < 1) occ = 1;
+    *grid = occ * ctx->sm_count;
+    return EIK_OK;
+}
+
+// one scheduler round: select -> cell-sweep -> round end
+template <typename T>
+static int enqueue_round(eik_ctx* ctx, int r, const CellArgs& ca, int sel_grid, int cgrid)
+{
+    k_select<<<sel_grid, 256, 0, ctx->stream>>>(ctx->ctl, ctx->wl0, ctx->wl1, ctx->proc_cell,
+                                                 ctx->proc_flags, ctx->key, ctx->state,
+                                                 (float)ctx->bin_width);
+    CK(cudaGetLastError());
+    int st;
+    if (r == 16) st = launch_cell<T, 16>(ctx, ca, cgrid);
+    else if (r == 8) st = launch_cell<T, 8>(ctx, ca, cgrid);
+    else st = launch_cell<T, 4>(ctx, ca, cgrid);
+    if (st) return st;
+    return EIK_OK;
+}
+
+__global__ void k_round_end_graph(Ctl* ctl, cudaGraphConditionalHandle h)
+{
+    cudaGraphSetConditional(h, round_end_body(ctl) ? 0u : 1u);
+}
+
+template <typename T>
+static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
+{
+    int cgrid = 0;
+    int st = cell_grid<T>(ctx, r, &cgrid);
+    if (st) return st;
+    if (ctx->loop_mode == 1) {
+        // host-driven loop (debug): one 8-byte readback per round
+        for (;;) {
+            CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            const Ctl& h = *ctx->ctl_host;
+            const uint32_t n = h.wl_count[h.cur];
+            if (n == 0) break;
+            if (h.rounds >= ctx->max_rounds) return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
+            const int sg = (int)((n + 255) / 256);
+            st = enqueue_round<T>(ctx, r, ca, sg, (int)(n < (uint32_t)cgrid ? n : (uint32_t)cgrid));
+            if (st) return st;
+            k_round_end<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
+            CK(cudaGetLastError());
+        }
+        return EIK_OK;
+    }
+    // device-resident loop: CUDA graph with a conditional WHILE node around one round
+    char keybuf[256];
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%p/%p/%g/%d", (int)sizeof(T), r, (long long)J,
+             ca.Vt, ca.Ht, ctx->bin_width, ctx->collect_stats);
+    if (!ctx->gexec || ctx->gkey != keybuf) {
+        if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
+        cudaGraph_t graph;
+        CK(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle handle;
+        CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = handle;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CK(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        // populate the body by capturing one round into it
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaStream_t saved = ctx->stream;
+        ctx->stream = cs;
+        CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        const int sg = (int)((J + 255) / 256 < (int64_t)ctx->sm_count * 4 ? (J + 255) / 256 : (int64_t)ctx->sm_count * 4);
+        st = enqueue_round<T>(ctx, r, ca, sg, cgrid);
+        k_round_end_graph<<<1, 1, 0, cs>>>(ctx->ctl, handle);
+        cudaGraph_t captured;
+        cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+        ctx->stream = saved;
+        cudaStreamDestroy(cs);
+        if (st) { cudaGraphDestroy(graph); return st; }
+        if (ce != cudaSuccess) { cudaGraphDestroy(graph); CK(ce); }
+        cudaError_t ie = cudaGraphInstantiate(&ctx->gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ie);
+        ctx->gkey = keybuf;
+    }
+    // the WHILE node evaluates its condition before the first iteration via the default
+    // value (1); an empty initial worklist is handled by the first k_select (no work) and
+    // k_round_end_graph (sets 0).
+    CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    return EIK_OK;
+}
+
+template <typename T>
+static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* mask,
+                      const void* q, void* U, int r)
+{
+    const int64_t n1 = n + 1;
+    const int cps = (int)((n1 + r - 1) / r);
+    const int64_t J = (int64_t)cps * cps * cps;
+    const int64_t r3 = (int64_t)r * r * r;
+    const int64_t P = J * r3;
+    const int64_t M = n1 * n1 * n1;
+    if (J >= (int64_t)1 << 31) return fail(ctx, EIK_EINVAL, "grid too large (J = %lld cells)", (long long)J);
+    int st = ensure_scratch(ctx, (size_t)P * sizeof(T), (size_t)J);
+    if (st) return st;
+    cudaStream_t s = ctx->stream;
+
+    Ctl init{};
+    init.kmin[0] = init.kmin[1] = KEY_INF;
+    init.max_rounds = ctx->max_rounds;
+    *ctx->ctl_host = init;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    CK(cudaMemcpyAsync(ctx->ctl, ctx->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+    const int G = ctx->sm_count * 8;
+    k_init_cells<<<G, 256, 0, s>>>(ctx->key, ctx->state, J);
+    Geom g{n1, cps, r};
+    k_ingest<T><<<G * 2, 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt, (T*)ctx->Ht,
+                                      ctx->key, ctx->state, ctx->ctl, P);
+    k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
+    CK(cudaGetLastError());
+    // input validation result (device-detected errors return before touching U_out)
+    CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (ctx->ctl_host->err & 1u) return fail(ctx, EIK_EINVAL, "F has a negative, NaN or infinite value");
+    if (ctx->ctl_host->err & 2u) return fail(ctx, EIK_EINVAL, "an exit value q is negative, NaN or infinite");
+    if (ctx->ctl_host->n_exits == 0) return fail(ctx, EIK_EINVAL, "no exit point (exit_mask is all zero)");
+    CK(cudaEventRecord(ctx->ev[1], s));
+
+    CellArgs ca;
+    ca.ctl = ctx->ctl;
+    ca.proc_cell = ctx->proc_cell;
+    ca.proc_flags = ctx->proc_flags;
+    ca.wl0 = ctx->wl0;
+    ca.wl1 = ctx->wl1;
+    ca.key = ctx->key;
+    ca.state = ctx->state;
+    const int ri = rindex_of(r);
+    ca.plane_tab = ctx->plane_tab[ri];
+    ca.plane_off = ctx->plane_off[ri];
+    ca.Vt = ctx->Vt;
+    ca.Ht = ctx->Ht;
+    ca.n1 = n1;
+    ca.cps = cps;
+    ca.stats = ctx->collect_stats;
+    st = run_loop<T>(ctx, r, J, ca);
+    if (st) return st;
+    CK(cudaEventRecord(ctx->ev[2], s));
+    CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (ctx->ctl_host->err & 4u)
+        return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
+    k_egress<T><<<G * 2, 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[3], s));
+    CK(cudaEventSynchronize(ctx->ev[3]));
+
+    const Ctl& hc = *ctx->ctl_host;
+    eik_stats& S = ctx->stats;
+    memset(&S, 0, sizeof S);
+    S.M = M;
+    S.padded_points = P;
+    S.J = J;
+    S.cells_per_side = cps;
+    S.cell_size = r;
+    S.precision = sizeof(T) == 4 ? EIK_F32 : EIK_F64;
+    S.point_updates = hc.updates;
+    S.point_writes = hc.writes;
+    S.cell_processings = hc.processings;
+    S.cell_sweeps = hc.sweeps;
+    S.real_points_processed = hc.real_pts;
+    S.rounds = hc.rounds;
+    S.max_worklist = hc.max_proc;
+    S.bytes_min = (uint64_t)((double)hc.real_pts * 2.0 * sizeof(T));
+    S.bytes_cell_alg = hc.processings * (uint64_t)((2 * r3 + 6 * r * r) * sizeof(T)) +
+                       hc.bytes_written * sizeof(T);
+    float ms;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]); S.ms_ingest = ms;
+    cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]); S.ms_loop = ms;
+    cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]); S.ms_egress = ms;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]); S.ms_total = ms;
+    ctx->have_stats = true;
+    return EIK_OK;
+}
+
+static int validate(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* mask,
+                    const void* q, void* U, int precision, int r)
+{
+    if (!ctx) return EIK_EINVAL;
+    ctx->err.clear();
+    if (!F || !mask || !q || !U) return fail(ctx, EIK_EINVAL, "null array pointer");
+    if (n < 1) return fail(ctx, EIK_EINVAL, "n must be >= 1 (got %lld)", (long long)n);
+    if (n > 100000) return fail(ctx, EIK_EINVAL, "n too large (%lld)", (long long)n);
+    if (!(h > 0) || !isfinite(h)) return fail(ctx, EIK_EINVAL, "h must be finite and > 0");
+    if (precision != EIK_F32 && precision != EIK_F64) return fail(ctx, EIK_EINVAL, "bad precision %d", precision);
+    if (rindex_of(r) < 0) return fail(ctx, EIK_EINVAL, "cell_size must be 4, 8 or 16 (got %d)", r);
+    return EIK_OK;
+}
+
+extern "C" int eik_solve(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
+                         const void* exit_vals, void* U_out, int precision, int cell_size)
+{
+    int st = validate(ctx, n, h, F, exit_mask, exit_vals, U_out, precision, cell_size);
+    if (st) return st;
+    CK(cudaSetDevice(ctx->device));
+    ctx->have_stats = false;
+    if (precision == EIK_F32) return solve_impl<float>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size);
+    return solve_impl<double>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size);
+}
+
+extern "C" int eik_solve_host(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
+                              const void* exit_vals, void* U_out, int precision, int cell_size)
+{
+    int st = validate(ctx, n, h, F, exit_mask, exit_vals, U_out, precision, cell_size);
+    if (st) return st;
+    CK(cudaSetDevice(ctx->device));
+    const size_t M = (size_t)(n + 1) * (n + 1) * (n + 1);
+    const size_t s = precision == EIK_F32 ? 4 : 8;
+    const size_t need = M * (3 * s + 1) + 256;
+    if (need > ctx->stage_bytes) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(ctx->stage);
+        ctx->stage = nullptr;
+        ctx->stage_bytes = 0;
+        CK(cudaMalloc(&ctx->stage, need));
+        ctx->stage_bytes = need;
+    }
+    char* base = (char*)ctx->stage;
+    void* dF = base;
+    void* dq = base + M * s;
+    void* dU = base + 2 * M * s;
+    uint8_t* dm = (uint8_t*)(base + 3 * M * s);
+    cudaStream_t sm = ctx->stream;
+    CK(cudaMemcpyAsync(dF, F, M * s, cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(dq, exit_vals, M * s, cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(dm, exit_mask, M, cudaMemcpyHostToDevice, sm));
+    st = eik_solve(ctx, n, h, dF, dm, dq, dU, precision, cell_size);
+    if (st) return st;
+    CK(cudaMemcpyAsync(U_out, dU, M * s, cudaMemcpyDeviceToHost, sm));
+    CK(cudaStreamSynchronize(sm));
+    return EIK_OK;
+}

@@ -1,0 +1,79 @@
+"""C-ABI boundary tests that need no GPU: the library builds/loads, exports every symbol that
+include/eik.h declares, and fails loudly (status + message, no crash) without a device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "eik.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(eik_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_expected_api():
+    names = _declared()
+    for need in ("eik_create", "eik_solve", "eik_destroy", "eik_solve_host", "eik_get_stats",
+                 "eik_last_error"):
+        assert need in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1306_4743_b200 as eik
+    for name in _declared():
+        assert hasattr(eik.lib, name), name
+    assert set(_declared()) == set(eik.EXPORTS)
+    assert eik.lib.eik_abi_version() == 1
+
+
+def test_lib_is_sm100a_cubin():
+    import subprocess
+    import paper_1306_4743_b200 as eik
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", eik.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_stats_struct_layout_matches_header():
+    import paper_1306_4743_b200 as eik
+    # 3*8 + 4*4 + 5*8 + 2*4 + 2*8 + 4*8 = 136 bytes
+    assert ctypes.sizeof(eik.EikStats) == 136
+
+
+def test_create_without_gpu_fails_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    import paper_1306_4743_b200 as eik
+    ctx = ctypes.c_void_p()
+    st = eik.lib.eik_create(ctypes.byref(ctx), 0, None)
+    assert st in (eik.EIK_ECUDA, eik.EIK_ENOTSUP)
+    assert ctx.value is None
+    assert eik.lib.eik_last_error(None)
+    with pytest.raises(eik.EikError):
+        eik.Solver()
+
+
+def test_null_safety():
+    import paper_1306_4743_b200 as eik
+    eik.lib.eik_destroy(None)  # NULL-safe
+    assert eik.lib.eik_solve(None, 8, 0.125, None, None, None, None, 0, 8) == eik.EIK_EINVAL
+    assert eik.lib.eik_solve_host(None, 8, 0.125, None, None, None, None, 0, 8) == eik.EIK_EINVAL
+    assert eik.lib.eik_set_option(None, 0, 1.0) == eik.EIK_EINVAL
+    assert eik.lib.eik_get_stats(None, None) == eik.EIK_EINVAL
+    assert eik.lib.eik_create(None, 0, None) == eik.EIK_EINVAL
+
+
+def test_product_path_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1306_4743_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "oracle.c" not in txt and \
+                       "liboracle" not in txt, f

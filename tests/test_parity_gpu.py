@@ -1,0 +1,206 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU fp64 FMM oracle on the same seeded
+inputs.  Bar (north_star): reachability/infinite masks bit-exact, exits
+exactly (dtype)q, fp64 max-abs <= 1e-10, fp32 max-rel <= 2e-5 over finite non-exit points."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32 = 2e-5
+
+
+@pytest.fixture(scope="module")
+def solver():
+    import paper_1306_4743_b200 as eik
+    s = eik.Solver(device=0)
+    yield s
+    s.close()
+
+
+def _gpu(solver, w, dtype, r, host=False):
+    import torch
+    F, m, q = w.as_dtype(dtype)
+    if host:
+        return solver.solve_host(F, m, q, cell_size=r, n=w.n)
+    U = solver.solve(torch.from_numpy(F).cuda(), torch.from_numpy(m).cuda(),
+                     torch.from_numpy(q).cuda(), cell_size=r, n=w.n)
+    return U.cpu().numpy()
+
+
+def assert_parity(U, U_orc, w, dtype):
+    U = U.astype(np.float64)
+    fin = np.isfinite(U_orc)
+    assert np.array_equal(np.isfinite(U), fin), \
+        f"mask mismatch at {np.argwhere(np.isfinite(U) != fin)[:5]}"
+    ex = w.exit_mask.astype(bool)
+    assert np.array_equal(U[ex], w.exit_vals[ex].astype(dtype).astype(np.float64))
+    nz = fin & ~ex
+    if not nz.any():
+        return 0.0
+    if dtype == np.float64:
+        err = np.abs(U[nz] - U_orc[nz]).max()
+        assert err <= TOL64, err
+    else:
+        err = (np.abs(U[nz] - U_orc[nz]) / U_orc[nz]).max()
+        assert err <= TOL32, err
+    return err
+
+
+_orc_cache = {}
+
+
+def oracle_U(w):
+    key = (w.name, w.n, w.meta.get("seed"))
+    if key not in _orc_cache:
+        _orc_cache[key] = oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals)
+    return _orc_cache[key]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("n", [16, 32, 64])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("r", [4, 8, 16])
+def test_reduced_configs(solver, name, n, dtype, r):
+    w = W.make(name, n)
+    assert_parity(_gpu(solver, w, dtype, r), oracle_U(w), w, dtype)
+
+
+@pytest.mark.parametrize("seed", range(10))
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_random_obstacles_ragged(solver, seed, dtype):
+    n = [5, 9, 15, 17, 23, 30, 33, 40, 47, 50][seed]   # (n+1) mod r != 0 for most r
+    w = W.random_instance(n, 100 + seed, p_wall=0.2, n_exits=1 + seed % 5,
+                          q_max=0.5 if seed % 2 else 0.0)
+    U_orc = oracle_U(w)
+    for r in (4, 8, 16):
+        assert_parity(_gpu(solver, w, dtype, r), U_orc, w, dtype)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 7])
+def test_tiny_grids(solver, n):
+    for seed in range(3):
+        w = W.random_instance(n, seed, p_wall=0.0, n_exits=1)
+        for r in (4, 8, 16):
+            assert_parity(_gpu(solver, w, np.float64, r), oracle_U(w), w, np.float64)
+
+
+def test_exits_on_cell_faces_edges_corners(solver):
+    n = 40
+    F = np.random.default_rng(1).uniform(0.5, 2.0, (n + 1,) * 3)
+    mask = np.zeros(F.shape, np.uint8)
+    for (i, j, k) in [(16, 5, 9), (15, 15, 3), (16, 16, 16), (31, 32, 33), (0, 40, 8), (40, 40, 40)]:
+        mask[k, j, i] = 1
+    q = np.zeros(F.shape)
+    q[mask.astype(bool)] = np.linspace(0, 0.3, mask.sum())
+    w = W.Workload("faces", n, F, mask, q)
+    U_orc = oracle_U(w)
+    for r in (4, 8, 16):
+        for dt in (np.float64, np.float32):
+            assert_parity(_gpu(solver, w, dt, r), U_orc, w, dt)
+
+
+def test_all_exit_grid_and_walls(solver):
+    n = 12
+    F = np.ones((n + 1,) * 3)
+    mask = np.ones(F.shape, np.uint8)
+    q = np.random.default_rng(0).uniform(0, 1, F.shape)
+    w = W.Workload("allexit", n, F, mask, q)
+    for dt in (np.float64, np.float32):
+        U = _gpu(solver, w, dt, 8)
+        assert np.array_equal(U, q.astype(dt))
+    # F = 0 everywhere except the exit: every other point unreachable
+    F = np.zeros((n + 1,) * 3)
+    mask = np.zeros(F.shape, np.uint8)
+    mask[3, 4, 5] = 1
+    w = W.Workload("walls", n, F, mask, np.zeros(F.shape))
+    U = _gpu(solver, w, np.float64, 4)
+    assert U[3, 4, 5] == 0 and np.isinf(U).sum() == U.size - 1
+
+
+def test_host_pointer_path(solver):
+    w = W.c2(32)
+    U_orc = oracle_U(w)
+    for dt in (np.float64, np.float32):
+        assert_parity(_gpu(solver, w, dt, 8, host=True), U_orc, w, dt)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("delta", [0.0, 0.05, 1e-6])
+def test_schedule_independence(mode, delta):
+    """Bin width, loop mode and cell size change the work, never the fixed point."""
+    import paper_1306_4743_b200 as eik
+    s = eik.Solver(device=0, loop_mode=mode, bin_width=delta)
+    for w in (W.c2(48), W.c3(48), W.c4(48)):
+        for r in (8, 16):
+            for dt in (np.float64, np.float32):
+                assert_parity(_gpu(s, w, dt, r), oracle_U(w), w, dt)
+    s.close()
+
+
+def test_stats_are_consistent(solver):
+    w = W.c1(64)
+    _gpu(solver, w, np.float64, 8)
+    st = solver.stats()
+    assert st["M"] == 65 ** 3 and st["J"] == 9 ** 3 and st["cell_size"] == 8
+    assert st["cell_processings"] >= st["J"]          # every cell is reached at least once
+    assert st["point_writes"] >= st["M"] - 1          # every non-exit point written >= once
+    assert st["point_updates"] >= st["point_writes"]
+    assert st["rounds"] >= 1 and st["ms_total"] > 0
+
+
+# ---------------------------------------------------------------- error convention -------
+def test_einval_leaves_output_untouched(solver):
+    import torch
+    import paper_1306_4743_b200 as eik
+    n = 8
+    shp = ((n + 1) ** 3,)
+    F = torch.ones(shp, dtype=torch.float64, device="cuda")
+    m = torch.zeros(shp, dtype=torch.uint8, device="cuda")
+    q = torch.zeros(shp, dtype=torch.float64, device="cuda")
+    m[0] = 1
+    U = torch.full(shp, 7.0, dtype=torch.float64, device="cuda")
+    L = eik.lib
+
+    def call(n_=n, h=0.125, F_=F, m_=m, q_=q, prec=1, r=8):
+        return L.eik_solve(solver._ctx, n_, h, F_.data_ptr() if F_ is not None else None,
+                           m_.data_ptr(), q_.data_ptr(), U.data_ptr(), prec, r)
+
+    assert call() == eik.EIK_OK
+    U.fill_(7.0)
+    bad = [dict(n_=0), dict(h=0.0), dict(h=float("inf")), dict(h=float("nan")), dict(prec=2),
+           dict(r=5), dict(r=32), dict(F_=None)]
+    for kw in bad:
+        assert call(**kw) == eik.EIK_EINVAL, kw
+        assert eik.lib.eik_last_error(solver._ctx)
+    for val in (-1.0, float("nan"), float("inf")):
+        F2 = F.clone()
+        F2[17] = val
+        assert call(F_=F2) == eik.EIK_EINVAL
+        q2 = q.clone()
+        q2[0] = val
+        assert call(q_=q2) == eik.EIK_EINVAL
+    assert call(m_=torch.zeros_like(m)) == eik.EIK_EINVAL     # no exit (R10)
+    assert bool((U == 7.0).all())
+    # -0 exit value is canonicalised to +0
+    q3 = q.clone()
+    q3[0] = -0.0
+    assert call(q_=q3) == eik.EIK_OK
+    assert float(U[0]) == 0.0 and not np.signbit(float(U[0]))
+
+
+# ---------------------------------------------------------------- full BASELINE sizes ----
+def test_full_c1(solver):
+    w = W.c1()
+    assert_parity(_gpu(solver, w, np.float64, 8), oracle_U(w), w, np.float64)
+
+
+def test_full_c2_all_variants(solver):
+    w = W.c2()
+    U_orc = oracle_U(w)
+    for dt in (np.float64, np.float32):
+        for r in (8, 16):
+            assert_parity(_gpu(solver, w, dt, r), U_orc, w, dt)

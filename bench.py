@@ -1,0 +1,322 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 cell-sweep Eikonal solver (pHCM hot path, arXiv 1306.4743).
+
+Metric (BASELINE.json): "Eikonal solve ms & gridpoints/s at 513^3; HBM GB/s as fraction of peak".
+Workload (default): C3 = n=512 (513^3 points), 8^3 checkerboard F in {1, 10}, corner exit,
+fp32, cell size 16 -- configs[2], the 513^3 configuration the metric is quoted on.
+A "step" is one full eik_solve (ingest -> device scheduler loop -> egress) over the resident
+inputs; value = gridpoints/s = M / (step time), summed over ranks (independent replicas).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C4|...] [--impl reference]
+
+N > 1: launched by torchrun, one process per GPU; the path does not shard ("replicas only",
+SURVEY 8(e)): each rank solves its own copy, no data-path collective; barrier + max over ranks.
+--impl reference: the CPU fp64 FMM oracle (the only "reference" this tier has) on the host
+cores, on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Eikonal solve ms & gridpoints/s at 513^3; HBM GB/s as fraction of peak"
+UNIT = "gridpoints/s"
+WORKLOADS = {
+    # name: (config, precision, cell size)
+    "C1": ("C1", "f64", 8), "C2": ("C2", "f32", 16), "C2d": ("C2", "f64", 8),
+    "C3": ("C3", "f32", 16), "C3d": ("C3", "f64", 16), "C4": ("C4", "f32", 16),
+    "C5": ("C5", "f32", 16),
+}
+DESC = {
+    "C1": "n=128 (129^3), F=1, centre exit",
+    "C2": "n=256 (257^3), F=1+0.5 sin(8pi x)sin(8pi y)sin(8pi z), centre exit",
+    "C3": "n=512 (513^3), 8^3 checkerboard F in {1,10}, exit (0,0,0)",
+    "C4": "n=512 (513^3), 8 F=0 walls with 4 random holes each, exit face z=0",
+    "C5": "n=1024 (1025^3), 32 Gaussian bumps, 64 random exits",
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p is not None:
+            time.sleep(0.15)
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6 and f[0].replace(".", "").isdigit():
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def make_inputs(cfg, prec, device, n=None):
+    """Seeded synthetic inputs of the config (workloads/), resident on `device`."""
+    import torch
+    import workloads as W
+    dt = torch.float32 if prec == "f32" else torch.float64
+    if cfg == "C5":
+        n = n or 1024
+        a, c, sig, ex = W.c5_params(n)
+        F = W.c5_field_torch(n, a, c, sig, device=device, dtype=torch.float64).to(dt).reshape(-1)
+        m = torch.zeros((n + 1) ** 3, dtype=torch.uint8, device=device)
+        idx = torch.tensor([i + (n + 1) * (j + (n + 1) * k) for (i, j, k) in ex], device=device)
+        m[idx] = 1
+        q = torch.zeros((n + 1) ** 3, dtype=dt, device=device)
+        return n, F.contiguous(), m, q
+    w = W.make(cfg, n)
+    Fh, mh, qh = w.as_dtype(np.float32 if prec == "f32" else np.float64)
+    return (w.n, torch.from_numpy(Fh.reshape(-1)).to(device), torch.from_numpy(mh.reshape(-1)).to(device),
+            torch.from_numpy(qh.reshape(-1)).to(device))
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
+
+
+def cpu_oracle_sample(cfg, n_sample):
+    """Time the fp64 FMM oracle as it stands on the same workload's formulas at reduced n."""
+    import oracle
+    import workloads as W
+    w = W.make(cfg, n_sample)
+    oracle.build()
+    t0 = time.perf_counter()
+    oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals)
+    dt = time.perf_counter() - t0
+    return w.M, dt
+
+
+def run_reference(args):
+    rank, _, ws = dist_env()
+    if rank != 0:
+        return 0
+    cfg, prec, r = WORKLOADS[args.config]
+    n_s = args.ref_n
+    import oracle
+    import workloads as W
+    oracle.build()
+    w = W.make(cfg, n_s)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    val = w.M / t
+    sample = (f"fp64 serial FMM oracle on the {cfg} formulas at n={n_s} ({w.M} points) per step "
+              f"(the {DESC[cfg].split(',')[0]} input would take minutes)")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(cfg, prec, r),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, prec, r, n=None):
+    n = n or {"C1": 128, "C2": 256, "C3": 512, "C4": 512, "C5": 1024}[cfg]
+    return {"workload": f"{cfg}: {DESC[cfg]}", "n": n, "points": (n + 1) ** 3, "cell_size": r,
+            "precision": prec, "solve": "eik_solve: ingest + device scheduler loop + egress",
+            "l2": "inputs (F + exit_mask + exit_vals) and tiles are > 4x the 126 MB L2; no flush"
+            if n >= 256 else "L2-resident (small config)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=None, help="override n (reduced size; not a bench line)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-n", type=int, default=128, help="oracle sample size for --impl reference")
+    ap.add_argument("--cpu-n", type=int, default=256, help="oracle sample size for cpu_baseline")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--bin-width", type=float, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_1306_4743_b200 as eik
+
+    rank, local, ws = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    cfg, prec, r = WORKLOADS[args.config]
+    n, F, m, q = make_inputs(cfg, prec, dev, args.n)
+    M = (n + 1) ** 3
+    s_bytes = 4 if prec == "f32" else 8
+    solver = eik.Solver(device=local, bin_width=args.bin_width)
+    U = torch.empty_like(F)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        solver.solve(F, m, q, cell_size=r, n=n, out=U)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    barrier()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            solver.solve(F, m, q, cell_size=r, n=n, out=U)
+            stats.append(solver.stats())
+        ev1.record(stream)
+        barrier()
+    t_ms = ev0.elapsed_time(ev1) / args.steps
+    if pg is not None:
+        tt = torch.tensor([t_ms], device=dev)
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = M * ws / (t_ms * 1e-3)
+
+    # roofline of the dominant kernel (cell sweep): algorithmic bytes / its device time
+    cell_ms = float(np.mean([s["ms_cell_device"] for s in stats]))
+    alg_bytes = float(np.mean([s["bytes_cell_alg"] for s in stats]))
+    launches = float(np.mean([s["cell_launches"] for s in stats]))
+    rounds = float(np.mean([s["rounds"] for s in stats]))
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (cell_ms * 1e-3) / 1e9 if cell_ms > 0 else None
+    # event-timed cross-check of the same kernel (host-loop mode, CUDA events around launches)
+    s2 = eik.Solver(device=local, loop_mode=1, bin_width=args.bin_width)
+    s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
+    s2.solve(F, m, q, cell_size=r, n=n, out=torch.empty_like(F))
+    st2 = s2.stats()
+    s2.close()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_{args.config}.json")
+    if os.path.exists(tp):   # ncu DRAM bytes of the cell kernel per processing x processings/launch
+        d = json.load(open(tp))["kcell_traffic"]
+        traffic = d["dram_bytes_per_processing"] * (stats[-1]["cell_processings"] / max(launches, 1))
+    st = stats[-1]
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": f"k_cell<{'float' if prec == 'f32' else 'double'},{r}>",
+            "alg_bytes_per_launch": alg_bytes / max(launches, 1),
+            "ms_per_launch_device": cell_ms / max(launches, 1),
+            "ms_per_launch_events": (st2["ms_cell_events"] / max(st2["cell_launches"], 1)),
+            "cell_share_of_step": cell_ms / t_ms, "peak_source": peak_src,
+            "alg_bytes_def": "per processing (2 r^3 + 6 r^2) s read + changed points * s written"}
+
+    # e2e: the same solve through the C ABI with pinned HOST buffers, copies inside the timing
+    e2e = None
+    if args.e2e_steps > 0:
+        Fh = F.cpu().pin_memory()
+        mh = m.cpu().pin_memory()
+        qh = q.cpu().pin_memory()
+        Uh = torch.empty_like(Fh).pin_memory()
+        solver.solve_host(Fh, mh, qh, cell_size=r, n=n, out=Uh)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            solver.solve_host(Fh, mh, qh, cell_size=r, n=n, out=Uh)
+        t_e = (time.perf_counter() - t0) / args.e2e_steps
+        if pg is not None:
+            tt = torch.tensor([t_e], device=dev)
+            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+            t_e = float(tt.item())
+        e2e = {"value": M * ws / t_e, "unit": UNIT, "ms_per_step": t_e * 1e3,
+               "h2d_bytes_per_step": int(Fh.numel() * Fh.element_size() + mh.numel() + qh.numel() * qh.element_size()),
+               "d2h_bytes_per_step": int(Uh.numel() * Uh.element_size()),
+               "timer": "host wall clock around the blocking C-ABI call (pinned buffers)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        Ms, secs = cpu_oracle_sample(cfg, args.cpu_n)
+        cpu = {"value": Ms / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"serial fp64 FMM oracle on the {cfg} formulas at n={args.cpu_n} "
+                         f"({Ms} points, {secs:.1f} s) on 1 of {os.cpu_count()} host cores"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": config_block(cfg, prec, r, n),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(args.steps * (4 + 3 * rounds)),
+            "clocks": clk.summary(),
+            "work": {"rounds": st["rounds"], "cell_processings": st["cell_processings"],
+                     "processings_per_cell": st["cell_processings"] / st["J"],
+                     "sweeps_per_cell": st["cell_sweeps"] / st["J"],
+                     "updates_per_point": st["point_updates"] / st["M"],
+                     "writes_per_point": st["point_writes"] / st["M"],
+                     "max_worklist": st["max_worklist"], "J": st["J"],
+                     "grid_pass_equivalents": st["real_points_processed"] / st["M"],
+                     "bytes_min_GBps": st["bytes_min"] / (t_ms * 1e-3) / 1e9,
+                     "ms_ingest": st["ms_ingest"], "ms_loop": st["ms_loop"], "ms_egress": st["ms_egress"]},
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

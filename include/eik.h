@@ -51,9 +51,20 @@ typedef enum {
                                 +inf = every queued cell each round.  [+inf]                    */
     EIK_OPT_MAX_ROUNDS = 1,  /* safety cap on scheduler rounds; exceeding it = EIK_EINTERNAL
                                 [1e9]                                                           */
-    EIK_OPT_LOOP_MODE = 2,   /* 0 = device-resident loop (CUDA graph WHILE node, no host
-                                round-trip per round); 1 = host-driven loop (debug) [0]          */
-    EIK_OPT_COLLECT_STATS = 3 /* 1 = count point updates/writes/sweeps on device [1]            */
+    EIK_OPT_LOOP_MODE = 2,   /* 0 = asynchronous persistent kernel (CTAs pull cells from a
+                                device ring; no rounds, no host round-trip);
+                                1 = bulk-synchronous rounds driven by the host (debug);
+                                2 = bulk-synchronous rounds in a CUDA graph WHILE node, no host
+                                round-trip per round [default]                                   */
+    EIK_OPT_COLLECT_STATS = 3, /* 1 = count point updates/writes/sweeps on device [1]           */
+    EIK_OPT_TIME_CELL_EVENTS = 4, /* 1 = (host loop mode only) bracket every cell-sweep kernel
+                                    launch with CUDA events; sum in eik_stats.ms_cell_events [0] */
+    EIK_OPT_ASYNC_DEFER = 5, /* async mode readiness test on a popped cell: 0 none, 1 defer
+                                while a neighbour runs [1], 2 also while a neighbour is queued
+                                with a smaller key, 3 ... with a key smaller by > bin width     */
+    EIK_OPT_MAX_SWEEPS = 6   /* sweeps per cell processing before the cell saves its active
+                                points and re-queues itself (bounds round length); 0 = until
+                                convergence [0]                                                  */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */
@@ -76,6 +87,11 @@ typedef struct {
     uint64_t bytes_cell_alg;    /* algorithmic cell-sweep bytes: per processing
                                    (2 r^3 + 6 r^2) s read + (changed points) s written          */
     double   ms_ingest, ms_loop, ms_egress, ms_total;   /* CUDA events on the ctx stream      */
+    double   ms_cell_device;    /* sum over rounds of the cell-sweep kernel's span (first CTA
+                                   start to last CTA end, %globaltimer), any loop mode          */
+    double   ms_cell_events;    /* sum of CUDA-event durations of the cell-sweep launches
+                                   (EIK_OPT_TIME_CELL_EVENTS in host loop mode), else 0         */
+    uint64_t cell_launches;     /* cell-sweep kernel launches that processed >= 1 cell        */
 } eik_stats;
 
 /* Create a context on `device`.  cuda_stream: a cudaStream_t to enqueue on (e.g. torch's
@@ -114,6 +130,13 @@ int eik_solve_host(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8
 
 /* Stats of the last successful solve.  EIK_EINVAL if ctx/out is NULL. */
 int eik_get_stats(const eik_ctx* ctx, eik_stats* out);
+
+/* Diagnostics of the last solve (for profiling; layout may change between ABI versions):
+ * out[0] sum of per-processing SM cycles, out[1] max, out[2] wavefront plane steps executed,
+ * out[3] processings, out[4 + s] number of processings that ran s sweeps (s = 31: >= 31),
+ * out[36..39] cycles in staging / plane-mask / plane steps / write-back, out[40] async-mode
+ * deferrals.  Copies min(n, 41) values.  EIK_EINVAL if ctx/out is NULL or n < 0. */
+int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n);
 
 /* Message of the last failing call on ctx (owned by ctx; valid until its next call).
  * eik_last_error(NULL) returns the message of the last failed eik_create. */

@@ -16,13 +16,14 @@ LIB_PATH = os.path.join(_PKG, "libeik.so")
 
 EIK_OK, EIK_EINVAL, EIK_ENOMEM, EIK_ECUDA, EIK_ENOTSUP, EIK_EINTERNAL = range(6)
 EIK_F32, EIK_F64 = 0, 1
-EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS = range(4)
+(EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS,
+ EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS) = range(7)
 STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
                 4: "EIK_ENOTSUP", 5: "EIK_EINTERNAL"}
 
 # every symbol include/eik.h declares (checked by tests/test_abi.py)
 EXPORTS = ("eik_create", "eik_set_stream", "eik_set_option", "eik_solve", "eik_solve_host",
-           "eik_get_stats", "eik_last_error", "eik_destroy", "eik_abi_version")
+           "eik_get_stats", "eik_get_debug", "eik_last_error", "eik_destroy", "eik_abi_version")
 
 
 class EikStats(ctypes.Structure):
@@ -35,7 +36,9 @@ class EikStats(ctypes.Structure):
                 ("rounds", ctypes.c_uint32), ("max_worklist", ctypes.c_uint32),
                 ("bytes_min", ctypes.c_uint64), ("bytes_cell_alg", ctypes.c_uint64),
                 ("ms_ingest", ctypes.c_double), ("ms_loop", ctypes.c_double),
-                ("ms_egress", ctypes.c_double), ("ms_total", ctypes.c_double)]
+                ("ms_egress", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("ms_cell_device", ctypes.c_double), ("ms_cell_events", ctypes.c_double),
+                ("cell_launches", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
@@ -64,6 +67,8 @@ def _load():
         f.restype = I
     lib.eik_get_stats.argtypes = [P, ctypes.POINTER(EikStats)]
     lib.eik_get_stats.restype = I
+    lib.eik_get_debug.argtypes = [P, P, I]
+    lib.eik_get_debug.restype = I
     lib.eik_last_error.argtypes = [P]
     lib.eik_last_error.restype = ctypes.c_char_p
     lib.eik_destroy.argtypes = [P]
@@ -88,7 +93,7 @@ class Solver:
     """One eik_ctx (device scratch reused across solves)."""
 
     def __init__(self, device: int = 0, stream=None, bin_width: float | None = None,
-                 loop_mode: int = 0, collect_stats: bool = True):
+                 loop_mode: int | None = None, collect_stats: bool = True):
         self._ctx = ctypes.c_void_p()
         st = lib.eik_create(ctypes.byref(self._ctx), device, stream)
         if st != EIK_OK:
@@ -96,7 +101,7 @@ class Solver:
         self.device = device
         if bin_width is not None:
             self.set_option(EIK_OPT_BIN_WIDTH, bin_width)
-        if loop_mode:
+        if loop_mode is not None:
             self.set_option(EIK_OPT_LOOP_MODE, loop_mode)
         if not collect_stats:
             self.set_option(EIK_OPT_COLLECT_STATS, 0)
@@ -170,6 +175,15 @@ class Solver:
         if st != EIK_OK:
             raise self._err(st)
         return out
+
+    def debug(self) -> dict:
+        import numpy as np
+        a = np.zeros(41, dtype=np.uint64)
+        lib.eik_get_debug(self._ctx, a.ctypes.data, 41)
+        return {"cycles_sum": int(a[0]), "cycles_max": int(a[1]), "plane_steps": int(a[2]),
+                "processings": int(a[3]), "sweep_hist": [int(x) for x in a[4:36]],
+                "cyc_stage": int(a[36]), "cyc_mask": int(a[37]), "cyc_steps": int(a[38]),
+                "cyc_writeback": int(a[39]), "defers": int(a[40])}
 
     def stats(self) -> dict:
         s = EikStats()

@@ -27,8 +27,13 @@ struct eik_ctx {
     // options
     double bin_width = INFINITY;
     uint32_t max_rounds = 1000000000u;
-    int loop_mode = 0;
+    int loop_mode = 2;
     int collect_stats = 1;
+    int time_cell_events = 0;
+    int async_defer = 1;
+    int max_sweeps = 0;
+    cudaEvent_t cev[2] = {nullptr, nullptr};
+    double ms_cell_events = 0;
     // scratch
     void* Vt = nullptr;
     void* Ht = nullptr;
@@ -39,7 +44,9 @@ struct eik_ctx {
     uint32_t* wl1 = nullptr;
     uint32_t* proc_cell = nullptr;
     uint32_t* proc_flags = nullptr;
+    uint32_t* pend = nullptr;
     size_t cell_cap = 0;
+    size_t ring_cap = 0;
     Ctl* ctl = nullptr;
     Ctl* ctl_host = nullptr;      // pinned
     // plane tables per r (index 0: r=4, 1: r=8, 2: r=16)
@@ -131,6 +138,7 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     CK(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&ctx->ctl_host, sizeof(Ctl)));
     for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&ctx->ev[i]));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreate(&ctx->cev[i]));
     const int rs[3] = {4, 8, 16};
     for (int t = 0; t < 3; ++t) {
         std::vector<uint16_t> tab;
@@ -148,6 +156,12 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     CK(cudaFuncSetAttribute(k_cell<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 8>()));
     CK(cudaFuncSetAttribute(k_cell<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 4>()));
     CK(cudaFuncSetAttribute(k_cell<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 4>()));
+    CK(cudaFuncSetAttribute(k_async<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
+    CK(cudaFuncSetAttribute(k_async<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 16>()));
+    CK(cudaFuncSetAttribute(k_async<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 8>()));
+    CK(cudaFuncSetAttribute(k_async<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 8>()));
+    CK(cudaFuncSetAttribute(k_async<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 4>()));
+    CK(cudaFuncSetAttribute(k_async<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 4>()));
     *out = ctx;
     return EIK_OK;
 }
@@ -156,7 +170,8 @@ static void free_scratch(eik_ctx* ctx)
 {
     cudaFree(ctx->Vt); cudaFree(ctx->Ht);
     cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
-    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags);
+    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend);
+    ctx->pend = nullptr;
     ctx->Vt = ctx->Ht = nullptr;
     ctx->key = ctx->state = ctx->wl0 = ctx->wl1 = ctx->proc_cell = ctx->proc_flags = nullptr;
     ctx->tile_bytes = ctx->cell_cap = 0;
@@ -174,6 +189,7 @@ extern "C" void eik_destroy(eik_ctx* ctx)
     cudaFreeHost(ctx->ctl_host);
     for (int t = 0; t < 3; ++t) { cudaFree(ctx->plane_tab[t]); cudaFree(ctx->plane_off[t]); }
     for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    for (int i = 0; i < 2; ++i) if (ctx->cev[i]) cudaEventDestroy(ctx->cev[i]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     (void)cudaGetLastError();
     delete ctx;
@@ -205,11 +221,23 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         ctx->max_rounds = value > 4e9 ? 0xffffffffu : (uint32_t)value;
         return EIK_OK;
     case EIK_OPT_LOOP_MODE:
-        if (value != 0 && value != 1) return fail(ctx, EIK_EINVAL, "loop mode must be 0 or 1");
+        if (value != 0 && value != 1 && value != 2)
+            return fail(ctx, EIK_EINVAL, "loop mode must be 0, 1 or 2");
         ctx->loop_mode = (int)value;
         return EIK_OK;
     case EIK_OPT_COLLECT_STATS:
         ctx->collect_stats = value != 0;
+        return EIK_OK;
+    case EIK_OPT_TIME_CELL_EVENTS:
+        ctx->time_cell_events = value != 0;
+        return EIK_OK;
+    case EIK_OPT_ASYNC_DEFER:
+        if (value < 0 || value > 3) return fail(ctx, EIK_EINVAL, "defer mode must be 0..3");
+        ctx->async_defer = (int)value;
+        return EIK_OK;
+    case EIK_OPT_MAX_SWEEPS:
+        if (!(value >= 0) || value > 1e6) return fail(ctx, EIK_EINVAL, "max sweeps must be >= 0");
+        ctx->max_sweeps = (int)value;
         return EIK_OK;
     default:
         return fail(ctx, EIK_EINVAL, "unknown option %d", option);
@@ -224,6 +252,15 @@ extern "C" int eik_get_stats(const eik_ctx* ctx, eik_stats* out)
         return EIK_EINVAL;
     }
     *out = ctx->stats;
+    return EIK_OK;
+}
+
+extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
+{
+    if (!ctx || !out || n < 0) return EIK_EINVAL;
+    const int m = n < 40 ? n : 40;
+    for (int i = 0; i < m; ++i) out[i] = ctx->ctl_host->dbg[i];
+    if (n > 40) out[40] = ctx->ctl_host->defers;
     return EIK_OK;
 }
 
@@ -244,10 +281,14 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
         ctx->tile_bytes = tile_bytes;
         CK(cudaMalloc(&ctx->key, J * 4));
         CK(cudaMalloc(&ctx->state, J * 4));
-        CK(cudaMalloc(&ctx->wl0, J * 4));
+        size_t cap = 1;
+        while (cap < J) cap <<= 1;
+        ctx->ring_cap = cap;
+        CK(cudaMalloc(&ctx->wl0, cap * 4));   // round-mode worklist / async-mode ring
         CK(cudaMalloc(&ctx->wl1, J * 4));
         CK(cudaMalloc(&ctx->proc_cell, J * 4));
         CK(cudaMalloc(&ctx->proc_flags, J * 4));
+        CK(cudaMalloc(&ctx->pend, J * 512));   // R^3 / 8 bytes per cell at r = 16
         ctx->cell_cap = J;
     }
     return EIK_OK;
@@ -277,17 +318,20 @@ static int cell_grid(eik_ctx* ctx, int r, int* grid)
 
 // one scheduler round: select -> cell-sweep -> round end
 template <typename T>
-static int enqueue_round(eik_ctx* ctx, int r, const CellArgs& ca, int sel_grid, int cgrid)
+static int enqueue_round(eik_ctx* ctx, int r, const CellArgs& ca, int sel_grid, int cgrid,
+                         bool time_events = false)
 {
     k_select<<<sel_grid, 256, 0, ctx->stream>>>(ctx->ctl, ctx->wl0, ctx->wl1, ctx->proc_cell,
                                                  ctx->proc_flags, ctx->key, ctx->state,
                                                  (float)ctx->bin_width);
     CK(cudaGetLastError());
+    if (time_events) CK(cudaEventRecord(ctx->cev[0], ctx->stream));
     int st;
     if (r == 16) st = launch_cell<T, 16>(ctx, ca, cgrid);
     else if (r == 8) st = launch_cell<T, 8>(ctx, ca, cgrid);
     else st = launch_cell<T, 4>(ctx, ca, cgrid);
     if (st) return st;
+    if (time_events) CK(cudaEventRecord(ctx->cev[1], ctx->stream));
     return EIK_OK;
 }
 
@@ -296,9 +340,42 @@ __global__ void k_round_end_graph(Ctl* ctl, cudaGraphConditionalHandle h)
     cudaGraphSetConditional(h, round_end_body(ctl) ? 0u : 1u);
 }
 
+template <typename T, int R>
+static int launch_async(eik_ctx* ctx, const CellArgs& a, int grid)
+{
+    k_async<T, R><<<grid, CellCfg<R>::NT, cell_smem_bytes<T, R>(), ctx->stream>>>(a);
+    CK(cudaGetLastError());
+    return EIK_OK;
+}
+
+template <typename T>
+static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
+{
+    int occ = 0;
+    cudaError_t e;
+    if (r == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 16>, CellCfg<16>::NT, cell_smem_bytes<T, 16>());
+    else if (r == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 8>, CellCfg<8>::NT, cell_smem_bytes<T, 8>());
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 4>, CellCfg<4>::NT, cell_smem_bytes<T, 4>());
+    CK(e);
+    if (occ < 1) occ = 1;
+    // every CTA is co-resident (grid = occupancy x SMs): idle CTAs only poll the ring
+    const int grid = occ * ctx->sm_count;
+    ca.qmask = (uint32_t)(ctx->ring_cap - 1);
+    ca.proc_limit = 4096ull * (unsigned long long)J + 1000000ull;
+    ca.defer = ctx->async_defer;
+    ca.defer_delta = isinf(ctx->bin_width) ? 0.f : (float)ctx->bin_width;
+    CK(cudaMemsetAsync(ctx->wl0, 0xff, ctx->ring_cap * 4, ctx->stream));
+    k_seed_queue<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(ctx->state, ctx->wl0, ctx->ctl, J);
+    CK(cudaGetLastError());
+    if (r == 16) return launch_async<T, 16>(ctx, ca, grid);
+    if (r == 8) return launch_async<T, 8>(ctx, ca, grid);
+    return launch_async<T, 4>(ctx, ca, grid);
+}
+
 template <typename T>
 static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
 {
+    if (ctx->loop_mode == 0) return run_async<T>(ctx, r, J, ca);
     int cgrid = 0;
     int st = cell_grid<T>(ctx, r, &cgrid);
     if (st) return st;
@@ -312,14 +389,21 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
             if (n == 0) break;
             if (h.rounds >= ctx->max_rounds) return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
             const int sg = (int)((n + 255) / 256);
-            st = enqueue_round<T>(ctx, r, ca, sg, (int)(n < (uint32_t)cgrid ? n : (uint32_t)cgrid));
+            const bool te = ctx->time_cell_events != 0;
+            st = enqueue_round<T>(ctx, r, ca, sg, (int)(n < (uint32_t)cgrid ? n : (uint32_t)cgrid), te);
             if (st) return st;
             k_round_end<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
             CK(cudaGetLastError());
+            if (te) {
+                CK(cudaEventSynchronize(ctx->cev[1]));
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, ctx->cev[0], ctx->cev[1]));
+                ctx->ms_cell_events += ms;
+            }
         }
         return EIK_OK;
     }
-    // device-resident loop: CUDA graph with a conditional WHILE node around one round
+    // loop mode 2: rounds in a CUDA graph with a conditional WHILE node around one round
     char keybuf[256];
     snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%p/%p/%g/%d", (int)sizeof(T), r, (long long)J,
              ca.Vt, ca.Ht, ctx->bin_width, ctx->collect_stats);
@@ -382,6 +466,8 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     Ctl init{};
     init.kmin[0] = init.kmin[1] = KEY_INF;
     init.max_rounds = ctx->max_rounds;
+    init.t_start = ~0ull;
+    ctx->ms_cell_events = 0;
     *ctx->ctl_host = init;
     CK(cudaEventRecord(ctx->ev[0], s));
     CK(cudaMemcpyAsync(ctx->ctl, ctx->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s));
@@ -390,7 +476,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     Geom g{n1, cps, r};
     k_ingest<T><<<G * 2, 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt, (T*)ctx->Ht,
                                       ctx->key, ctx->state, ctx->ctl, P);
-    k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
+    if (ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
     // input validation result (device-detected errors return before touching U_out)
     CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
@@ -401,6 +487,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     CK(cudaEventRecord(ctx->ev[1], s));
 
     CellArgs ca;
+    memset(&ca, 0, sizeof ca);
     ca.ctl = ctx->ctl;
     ca.proc_cell = ctx->proc_cell;
     ca.proc_flags = ctx->proc_flags;
@@ -413,6 +500,8 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.plane_off = ctx->plane_off[ri];
     ca.Vt = ctx->Vt;
     ca.Ht = ctx->Ht;
+    ca.max_sweeps = ctx->max_sweeps;
+    ca.pend = ctx->pend;
     ca.n1 = n1;
     ca.cps = cps;
     ca.stats = ctx->collect_stats;
@@ -423,6 +512,8 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     CK(cudaStreamSynchronize(s));
     if (ctx->ctl_host->err & 4u)
         return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
+    if (ctx->ctl_host->abort)
+        return fail(ctx, EIK_EINTERNAL, "processing limit exceeded (async scheduler)");
     k_egress<T><<<G * 2, 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[3], s));
@@ -452,6 +543,9 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     cudaEventElapsedTime(&ms, ctx->ev[1], ctx->ev[2]); S.ms_loop = ms;
     cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]); S.ms_egress = ms;
     cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]); S.ms_total = ms;
+    S.ms_cell_device = hc.cell_ns * 1e-6;
+    S.ms_cell_events = ctx->ms_cell_events;
+    S.cell_launches = hc.cell_launches;
     ctx->have_stats = true;
     return EIK_OK;
 }

@@ -64,6 +64,59 @@ __device__ __forceinline__ T local_solve(T mx, T my, T mz, T hf)
     return a1 + t;
 }
 
+// The same solve with the two- and three-sided candidates evaluated side by side and then
+// selected (shorter dependent chain: both square roots issue together).  d2, d3 are clamped to
+// hf, which changes nothing when a branch is taken (it requires d2 < hf, resp. d3 < t2 <= hf)
+// and keeps every operand finite.  Identical results to local_solve in every case.
+__device__ __forceinline__ float sqrt_fast(float x) { return __fsqrt_rn(x); }
+__device__ __forceinline__ double sqrt_fast(double x) { return __dsqrt_rn(x); }
+
+// fp32: sqrt.approx (MUFU, ~1 ulp); the shifted form only multiplies its error by O(hf), so
+// the effect on U is an ulp of hf (reading R14: fp32 arithmetic throughout).  fp64: IEEE.
+__device__ __forceinline__ float sqrt_approx(float x)
+{
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ double sqrt_approx(double x) { return __dsqrt_rn(x); }
+
+template <typename T>
+__device__ __forceinline__ T local_solve_fast(T mx, T my, T mz, T hf)
+{
+    const T lo = fmin(mx, my), hi = fmax(mx, my);
+    const T a1 = fmin(lo, mz);
+    const T a3 = fmax(hi, mz);
+    const T a2 = fmax(lo, fmin(hi, mz));
+    const T d2 = fmin(a2 - a1, hf);
+    const T d3 = fmin(a3 - a1, hf);
+    const T hh = hf * hf;
+    const T t2 = (d2 + sqrt_approx(fmax(T(2) * hh - d2 * d2, T(0)))) * T(0.5);
+    const T e = d3 - d2;
+    const T t3 = (d2 + d3 + sqrt_approx(fmax(T(3) * hh - (d2 * d2 + d3 * d3 + e * e), T(0)))) * T(1.0 / 3.0);
+    T t = hf;
+    if (hf > d2) t = (t2 > d3) ? t3 : t2;
+    return a1 + t;
+}
+
+template <typename T>
+__device__ __forceinline__ T local_solve_par(T mx, T my, T mz, T hf)
+{
+    const T lo = fmin(mx, my), hi = fmax(mx, my);
+    const T a1 = fmin(lo, mz);
+    const T a3 = fmax(hi, mz);
+    const T a2 = fmax(lo, fmin(hi, mz));
+    const T d2 = fmin(a2 - a1, hf);
+    const T d3 = fmin(a3 - a1, hf);
+    const T hh = hf * hf;
+    const T t2 = (d2 + sqrt_fast(fmax(T(2) * hh - d2 * d2, T(0)))) * T(0.5);
+    const T e = d3 - d2;
+    const T t3 = (d2 + d3 + sqrt_fast(fmax(T(3) * hh - (d2 * d2 + d3 * d3 + e * e), T(0)))) * T(1.0 / 3.0);
+    T t = hf;
+    if (hf > d2) t = (t2 > d3) ? t3 : t2;
+    return a1 + t;
+}
+
 // --------------------------------------------------------------------------------------
 // device-side control block (one per ctx)
 // --------------------------------------------------------------------------------------
@@ -79,9 +132,27 @@ struct Ctl {
     uint32_t err;           // 1: bad F, 2: bad q, 4: internal (max rounds)
     uint32_t n_exits;
     unsigned long long updates, writes, processings, sweeps, real_pts, bytes_written;
+    unsigned long long t_start, t_end;     // this round's cell-kernel span (%globaltimer ns)
+    unsigned long long cell_ns, cell_launches;
+    uint32_t q_head, q_tail, pending, abort;   // async mode ring + work counter
+    unsigned long long defers;
+    // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
+    // steps executed, [3] processings, [4..35] histogram of sweeps per processing (31 = >=31)
+    unsigned long long dbg[40];   // [36] stage, [37] plane-mask, [38] steps, [39] write-back cycles
 };
 
-enum : uint32_t { FLAG_INIT = 64u };   // state bit: activate every point (first processing)
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+enum : uint32_t {
+    FLAG_INIT = 64u,    // state bit: activate every point (first processing)
+    FLAG_CONT = 128u    // state bit: the cell stopped at the sweep cap; its active points are
+                        // saved in CellArgs::pend and are restored by the next processing
+};
 
 struct Geom {
     int64_t n1;        // n + 1 points per side
@@ -239,6 +310,12 @@ __device__ __forceinline__ bool round_end_body(Ctl* ctl)
     ctl->rounds += 1;
     if (ctl->proc_count > ctl->max_proc) ctl->max_proc = ctl->proc_count;
     ctl->processings += ctl->proc_count;
+    if (ctl->proc_count > 0 && ctl->t_end > ctl->t_start) {
+        ctl->cell_ns += ctl->t_end - ctl->t_start;
+        ctl->cell_launches += 1;
+    }
+    ctl->t_start = ~0ull;
+    ctl->t_end = 0;
     ctl->proc_count = 0;
     ctl->wl_count[cur] = 0;
     ctl->kmin[cur] = KEY_INF;
@@ -259,31 +336,44 @@ template <int R> struct CellCfg {
     static constexpr int RP = R + 2;
     static constexpr int RP2 = RP * RP;
     static constexpr int BOX = RP * RP * RP;
-    static constexpr int NPL = 3 * R - 2;                                 // wavefront planes
-    static constexpr int NT = R == 16 ? 192 : (R == 8 ? 64 : 32);          // >= largest plane
+    static constexpr int NPL = 3 * R - 2;                            // wavefront planes
+    static constexpr int MAXP = R == 16 ? 192 : (R == 8 ? 48 : 12);  // largest plane
+    static constexpr int NT = (MAXP + 31) / 32 * 32;                 // one plane point / thread
+    static constexpr int MINB = R == 16 ? 4 : 8;                     // CTAs per SM target
 };
+
+template <typename T, int R> struct MinBlocks { static constexpr int value = CellCfg<R>::MINB; };
+template <> struct MinBlocks<double, 16> { static constexpr int value = 2; };
 
 template <typename T, int R>
 constexpr size_t cell_smem_bytes()
 {
-    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + CellCfg<R>::R3;
+    // V box + hf + plane table (uint16) + active bytes
+    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + 3 * CellCfg<R>::R3;
 }
 
 struct CellArgs {
     Ctl* ctl;
-    const uint32_t* proc_cell;
+    const uint32_t* proc_cell;   // round mode: this round's cells
     const uint32_t* proc_flags;
-    uint32_t* wl0;
+    uint32_t* wl0;               // round mode: worklists; async mode: wl0 = queue ring
     uint32_t* wl1;
+    uint32_t qmask;              // async mode: ring capacity - 1 (power of two)
     uint32_t* key;
     uint32_t* state;
-    const uint16_t* plane_tab;   // R^3 entries (a | b<<4 | c<<8) sorted by a+b+c
+    const uint16_t* plane_tab;   // R^3 entries (a | b<<4 | c<<8) sorted by plane a+b+c
     const int32_t* plane_off;    // NPL + 1 offsets
     void* Vt;
     const void* Ht;
     int64_t n1;
     int32_t cps;
     int32_t stats;
+    unsigned long long proc_limit;   // async mode: abort after this many processings
+    int32_t defer;                   // async mode: readiness deferral (0 off, 1 running
+                                     // neighbours, 2 + smaller-key queued, 3 + key - delta)
+    float defer_delta;
+    int32_t max_sweeps;              // sweeps per processing before continuing later (0: none)
+    uint32_t* pend;                  // J x R^3/32 saved active bits (FLAG_CONT)
 };
 
 // preferred sweep directions from the inflow faces (reading R20): a direction
@@ -301,201 +391,554 @@ __device__ __forceinline__ uint32_t pref_dirs(uint32_t faces)
     return m;
 }
 
+// Shared-memory state of one cell processing (static part; the big arrays are dynamic).
+template <int R> struct CellShared {
+    int32_t off[CellCfg<R>::NPL + 1];  // plane offsets into the plane table
+    unsigned long long plane[2];
+    uint32_t face_min[6];              // Eq. (3) min newly-updated inflow value per face
+    uint32_t face_flag;                // faces whose neighbour is currently downwind
+    unsigned long long stat[3];
+    uint32_t cell, flags;              // async mode broadcast
+    uint32_t cont;                     // processing stopped at the sweep cap
+    uint32_t cont_key;                 // min V over the points still active (key bits)
+};
+
+// dynamic shared memory carve-up
+template <typename T, int R> struct CellSmem {
+    T* V;          // (R+2)^3 box incl. halo faces
+    T* H;          // R^3 hf (sign bit set = point changed in this processing)
+    uint16_t* tab; // plane table
+    uint8_t* act;  // R^3 active flags (Alg. 2)
+    __device__ explicit CellSmem(unsigned char* raw)
+    {
+        V = reinterpret_cast<T*>(raw);
+        H = V + CellCfg<R>::BOX;
+        tab = reinterpret_cast<uint16_t*>(H + CellCfg<R>::R3);
+        act = reinterpret_cast<uint8_t*>(tab + CellCfg<R>::R3);
+    }
+};
+
+// once per CTA: plane table and offsets into shared memory
 template <typename T, int R>
-__global__ void __launch_bounds__(CellCfg<R>::NT)
+__device__ __forceinline__ void cell_init_tables(const CellArgs& A, CellShared<R>& S, CellSmem<T, R>& M)
+{
+    using C = CellCfg<R>;
+    for (int s = threadIdx.x; s <= C::NPL; s += C::NT) S.off[s] = __ldg(&A.plane_off[s]);
+    for (int e = threadIdx.x; e < C::R3; e += C::NT) M.tab[e] = __ldg(&A.plane_tab[e]);
+}
+
+// Process one cell to convergence (HCM "perform modified LSM on c until convergence",
+// Alg. 1 line 6): stage the tile and its one-point halo N(c) (boundary data of
+// c~ = c u N(c)), run gated Gauss-Seidel sweeps, write back changed values.  On return the
+// face summaries (face_flag, face_min) are in S; the caller re-activates neighbours.
+//
+// A sweep in direction d visits the wavefront planes s = i' + j' + k' = 0 .. 3R-3 (primes =
+// coordinates reflected per d) in order: the exact Gauss-Seidel ordering of that sweep
+// (Detrixhe et al. planes).  The points of a plane are independent and are
+// packed onto consecutive threads through a shared plane table (one point per thread).  A
+// step is latency-bound (it depends on the previous plane), so its chain is kept short and
+// free of shared atomics: the next step's table entry and hf are prefetched, activity is one
+// byte per point written with plain stores (several writers only ever store 1), "changed"
+// is the sign bit of the point's hf, the two- and three-sided candidates of the local solve
+// are evaluated side by side, the Eq. (3) face minima are kept per thread and reduced once
+// per processing, and the step ends in one __syncthreads_or that also reports forward
+// activations.  LSM gating (Alg. 2); planes without active points are skipped
+// without a barrier.  Tile traffic bypasses L1 (ld/st .cg): other CTAs update neighbouring
+// tiles concurrently in the asynchronous scheduler.
+template <typename T, int R>
+__device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S,
+                                             CellSmem<T, R>& M, uint32_t c, uint32_t flags,
+                                             unsigned long long& n_sweeps_out)
+{
+    using C = CellCfg<R>;
+    constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
+    const int tid = threadIdx.x;
+    T* Vt = reinterpret_cast<T*>(A.Vt);
+    const T* Ht = reinterpret_cast<const T*>(A.Ht);
+    T* sV = M.V;
+    T* sH = M.H;
+    uint8_t* sA = M.act;
+    const int cps = A.cps;
+    const T INF = dinf<T>();
+    const int cx = (int)(c % (uint32_t)cps), cy = (int)((c / (uint32_t)cps) % (uint32_t)cps),
+              cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
+    const int64_t base = (int64_t)c * R3;
+    if (tid < 6) S.face_min[tid] = KEY_INF;
+    if (tid == 0) { S.face_flag = 0; S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF; }
+    long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0;
+    constexpr int NWB = R3 / 32;   // saved-bitmask words
+
+    // ---- stage V, hf and the initial activity (coalesced) ----
+    const bool init = flags & FLAG_INIT;
+#pragma unroll 4
+    for (int e = tid; e < R3; e += NT) {
+        const int a = e % R, b = (e / R) % R, d = e / (R * R);
+        sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = __ldcg(&Vt[base + e]);
+        sH[e] = __ldcg(&Ht[base + e]);
+        const bool on = init || ((flags & 1u) && a == 0) || ((flags & 2u) && a == R - 1) ||
+                        ((flags & 4u) && b == 0) || ((flags & 8u) && b == R - 1) ||
+                        ((flags & 16u) && d == 0) || ((flags & 32u) && d == R - 1);
+        sA[e] = on ? 1 : 0;
+    }
+    if (flags & FLAG_CONT) {       // restore the active points saved at the sweep cap
+        __syncthreads();
+        for (int w = tid; w < NWB; w += NT) {
+            uint32_t x = __ldcg(&A.pend[(int64_t)c * NWB + w]);
+            while (x) {
+                const int l = __ffs(x) - 1;
+                x &= x - 1;
+                sA[32 * w + l] = 1;
+            }
+        }
+    }
+    // ---- halo N(c): 6 faces of r^2 from the neighbour tiles (+inf outside the grid) ----
+    for (int e = tid; e < 6 * R * R; e += NT) {
+        const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
+        int hx, hy, hz, sa, sb, sd;
+        int64_t nc;
+        bool ex;
+        switch (f) {
+        case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
+        case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
+        case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
+        case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
+        case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
+        default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
+        }
+        T hv = INF;
+        if (ex) hv = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
+        sV[(hx + 1) + RP * (hy + 1) + RP2 * (hz + 1)] = hv;
+    }
+    __syncthreads();
+    const long long tc1 = clock64();
+
+    // ---- gated GS sweeps in wavefront order until no point is active ----
+    const uint32_t pref = init ? 0u : pref_dirs(flags & 63u);
+    int gi = 0;
+    bool pref_phase = pref != 0;
+    uint32_t nsweeps = 0;
+    uint32_t nupd = 0, nwr = 0;
+    for (int sw = 0;; ++sw) {
+        int dir;
+        {
+            const uint32_t gray = 0x45762310u;   // Gray cycle 0,1,3,2,6,7,5,4 (nibbles)
+            if (pref_phase) {
+                while (gi < 8 && !(pref & (1u << ((gray >> (4 * gi)) & 15u)))) ++gi;
+                if (gi < 8) { dir = (gray >> (4 * gi)) & 15u; ++gi; }
+                else { pref_phase = false; dir = 0; gi = 1; }
+            } else {
+                dir = (gray >> (4 * gi)) & 15u;
+                gi = (gi + 1) & 7;
+            }
+        }
+        const bool fx = dir & 1, fy = dir & 2, fz = dir & 4;
+        const long long tm0 = clock64();
+        // the set of planes (in this direction) holding active points
+        {
+            unsigned long long pm = 0;
+            const uint32_t* sA32 = reinterpret_cast<const uint32_t*>(sA);
+            for (int wd = tid; wd < R3 / 4; wd += NT) {
+                uint32_t x = sA32[wd];
+                while (x) {
+                    const int e = 4 * wd + ((__ffs(x) - 1) >> 3);
+                    x &= x - 1;
+                    const int a = e % R, b = (e / R) % R, d = e / (R * R);
+                    pm |= 1ull << ((fx ? R - 1 - a : a) + (fy ? R - 1 - b : b) + (fz ? R - 1 - d : d));
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) pm |= __shfl_xor_sync(0xffffffffu, pm, o);
+            if ((tid & 31) == 0 && pm) atomicOr(&S.plane[sw & 1], pm);
+        }
+        __syncthreads();
+        const unsigned long long pm = S.plane[sw & 1];
+        if (tid == 0) S.plane[(sw + 1) & 1] = 0;
+        const long long tm1 = clock64();
+        tmask += tm1 - tm0;
+        if (pm == 0ull) break;
+        if (A.max_sweeps > 0 && nsweeps >= (uint32_t)A.max_sweeps) {
+            // sweep cap reached with points still active: save them and continue in a later
+            // processing (the cell re-queues itself; correctness is unaffected, values only
+            // decrease and every active point is eventually processed)
+            uint32_t km = KEY_INF;
+            for (int w = tid; w < NWB; w += NT) {
+                uint32_t bits = 0;
+                for (int l = 0; l < 32; ++l) {
+                    const int e = 32 * w + l;
+                    if (sA[e]) {
+                        bits |= 1u << l;
+                        const int a = e % R, b = (e / R) % R, d = e / (R * R);
+                        km = min(km, key_bits(sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)]));
+                    }
+                }
+                __stcg(&A.pend[(int64_t)c * NWB + w], bits);
+            }
+            for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
+            if ((tid & 31) == 0) atomicMin(&S.cont_key, km);
+            if (tid == 0) S.cont = 1;
+            break;
+        }
+        ++nsweeps;
+        bool fwd = false;
+        int s = __ffsll((long long)pm) - 1;
+        // prefetch: the point this thread owns at plane sp and its hf
+        int pn = -1;
+        T hn = INF;
+        auto prefetch = [&](int sp) {
+            pn = -1;
+            if (sp < NPL) {
+                const int e = S.off[sp] + tid;
+                if (e < S.off[sp + 1]) {
+                    const uint32_t ent = M.tab[e];
+                    const int i = fx ? R - 1 - (int)(ent & 15u) : (int)(ent & 15u);
+                    const int j = fy ? R - 1 - (int)((ent >> 4) & 15u) : (int)((ent >> 4) & 15u);
+                    const int k = fz ? R - 1 - (int)(ent >> 8) : (int)(ent >> 8);
+                    pn = i + R * j + R * R * k;
+                    hn = sH[pn];
+                }
+            }
+        };
+        prefetch(s);
+        for (; s < NPL; ++s) {
+            const bool has = (pm >> s) & 1ull;
+            if (!has && !fwd) {
+                if ((pm >> s) == 0ull) break;
+                prefetch(s + 1);
+                continue;
+            }
+            const int p = pn;
+            const T hs = hn;
+            prefetch(s + 1);   // independent of this step's results
+            bool myfwd = false;
+            if (p >= 0 && sA[p]) {
+                sA[p] = 0;                                                 // Alg. 2 line 4
+                const T hf = fabs(hs);
+                const int i = p % R, j = (p / R) % R, k = p / (R * R);
+                const int q = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
+                const T v = sV[q];
+                const T xm = sV[q - 1], xp = sV[q + 1];
+                const T ym = sV[q - RP], yp = sV[q + RP];
+                const T zm = sV[q - RP2], zp = sV[q + RP2];
+                const T mx = fmin(xm, xp), my = fmin(ym, yp), mz = fmin(zm, zp);
+                if (hf < INF && fmin(mx, fmin(my, mz)) < v) {              // fixed / no gain
+                    ++nupd;
+                    const T u = local_solve_fast<T>(mx, my, mz, hf);        // line 5
+                    if (u < v) {                                             // line 6
+                        sV[q] = u;                                           // line 7
+                        if (hs > T(0)) sH[p] = -hs;                          // mark changed
+                        ++nwr;
+                        // lines 8-13: activate larger neighbours (predicated stores; the
+                        // cross-border "currently downwind" test is done once per processing)
+                        if (xm > u && i > 0) sA[p - 1] = 1;
+                        if (xp > u && i < R - 1) sA[p + 1] = 1;
+                        if (ym > u && j > 0) sA[p - R] = 1;
+                        if (yp > u && j < R - 1) sA[p + R] = 1;
+                        if (zm > u && k > 0) sA[p - R * R] = 1;
+                        if (zp > u && k < R - 1) sA[p + R * R] = 1;
+                        myfwd = ((fx ? xm : xp) > u) | ((fy ? ym : yp) > u) | ((fz ? zm : zp) > u);
+                    }
+                }
+            }
+            fwd = __syncthreads_or(myfwd);
+            ++nsteps;
+        }
+        tstep += clock64() - tm1;
+    }
+    const long long tc2 = clock64();
+
+    // ---- face summaries (Eq. (3)): face f is currently downwind iff a border
+    // point changed in this processing and ended below its outside neighbour (the staged
+    // halo value, an upper bound of the current one: P:718 redundant tags are harmless); the
+    // cell key candidate is the smallest such value (A_new of Eq. (3)).
+    {
+        uint32_t fm = KEY_INF;
+        int f_prev = -1;
+        for (int e = tid; e < 6 * R * R; e += NT) {
+            const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
+            int a, b, d, ha, hb, hd;
+            switch (f) {
+            case 0: a = 0; b = u; d = v; ha = -1; hb = b; hd = d; break;
+            case 1: a = R - 1; b = u; d = v; ha = R; hb = b; hd = d; break;
+            case 2: a = u; b = 0; d = v; ha = a; hb = -1; hd = d; break;
+            case 3: a = u; b = R - 1; d = v; ha = a; hb = R; hd = d; break;
+            case 4: a = u; b = v; d = 0; ha = a; hb = b; hd = -1; break;
+            default: a = u; b = v; d = R - 1; ha = a; hb = b; hd = R; break;
+            }
+            if (f != f_prev) {
+                if (f_prev >= 0 && fm != KEY_INF) { atomicMin(&S.face_min[f_prev], fm); atomicOr(&S.face_flag, 1u << f_prev); }
+                fm = KEY_INF;
+                f_prev = f;
+            }
+            const int pp = a + R * b + R * R * d;
+            if (sH[pp] < T(0)) {
+                const T val = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
+                const T out = sV[(ha + 1) + RP * (hb + 1) + RP2 * (hd + 1)];
+                if (val < out) fm = min(fm, key_bits(val));
+            }
+        }
+        if (f_prev >= 0 && fm != KEY_INF) { atomicMin(&S.face_min[f_prev], fm); atomicOr(&S.face_flag, 1u << f_prev); }
+    }
+    __syncthreads();
+
+    // ---- write back changed values only (coalesced) ----
+    unsigned long long nw = 0;
+    for (int e = tid; e < R3; e += NT) {
+        if (sH[e] < T(0)) {
+            const int a = e % R, b = (e / R) % R, d = e / (R * R);
+            __stcg(&Vt[base + e], sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)]);
+            ++nw;
+        }
+    }
+    if (A.stats) {
+        unsigned long long u64 = nupd, w64 = nwr;
+        for (int o = 16; o > 0; o >>= 1) {
+            u64 += __shfl_xor_sync(0xffffffffu, u64, o);
+            w64 += __shfl_xor_sync(0xffffffffu, w64, o);
+            nw += __shfl_xor_sync(0xffffffffu, nw, o);
+        }
+        if ((tid & 31) == 0) {
+            atomicAdd(&S.stat[0], u64);
+            atomicAdd(&S.stat[1], w64);
+            atomicAdd(&S.stat[2], nw);
+        }
+    }
+    n_sweeps_out = nsweeps;
+    if (tid == 0 && A.stats) {
+        atomicAdd(&A.ctl->dbg[36], (unsigned long long)(tc1 - tc0));
+        atomicAdd(&A.ctl->dbg[37], (unsigned long long)tmask);
+        atomicAdd(&A.ctl->dbg[38], (unsigned long long)tstep);
+        atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - tc2));
+        atomicAdd(&A.ctl->dbg[2], (unsigned long long)nsteps);
+    }
+}
+
+// neighbour cell across face f of c, or -1 outside the grid
+__device__ __forceinline__ int64_t face_neighbour(uint32_t c, int f, int cps)
+{
+    const int cx = (int)(c % (uint32_t)cps), cy = (int)((c / (uint32_t)cps) % (uint32_t)cps),
+              cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
+    switch (f) {
+    case 0: return cx > 0 ? (int64_t)c - 1 : -1;
+    case 1: return cx < cps - 1 ? (int64_t)c + 1 : -1;
+    case 2: return cy > 0 ? (int64_t)c - cps : -1;
+    case 3: return cy < cps - 1 ? (int64_t)c + cps : -1;
+    case 4: return cz > 0 ? (int64_t)c - (int64_t)cps * cps : -1;
+    default: return cz < cps - 1 ? (int64_t)c + (int64_t)cps * cps : -1;
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void cell_stats(const CellArgs& A, CellShared<R>& S, uint32_t c,
+                                           unsigned long long nsweeps)
+{
+    Ctl* ctl = A.ctl;
+    const int cps = A.cps;
+    const int64_t n1 = A.n1;
+    const int cx = (int)(c % (uint32_t)cps), cy = (int)((c / (uint32_t)cps) % (uint32_t)cps),
+              cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
+    atomicAdd(&ctl->updates, S.stat[0]);
+    atomicAdd(&ctl->writes, S.stat[1]);
+    atomicAdd(&ctl->bytes_written, S.stat[2]);
+    atomicAdd(&ctl->sweeps, nsweeps);
+    const int64_t rx = (n1 - (int64_t)cx * R) < R ? (n1 - (int64_t)cx * R) : R;
+    const int64_t ry = (n1 - (int64_t)cy * R) < R ? (n1 - (int64_t)cy * R) : R;
+    const int64_t rz = (n1 - (int64_t)cz * R) < R ? (n1 - (int64_t)cz * R) : R;
+    atomicAdd(&ctl->real_pts, (unsigned long long)(rx * ry * rz));
+    atomicAdd(&ctl->dbg[4 + (nsweeps < 31 ? nsweeps : 31)], 1ull);
+}
+
+// ---- round mode: one CTA per cell of this round's list (grid-stride) ------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(CellCfg<R>::NT, MinBlocks<T, R>::value)
 k_cell(CellArgs A)
 {
     using C = CellCfg<R>;
-    constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* sV = reinterpret_cast<T*>(smem_raw);               // (R+2)^3 box incl. halo faces
-    T* sH = sV + C::BOX;                                  // R^3 hf
-    uint8_t* sF = reinterpret_cast<uint8_t*>(sH + R3);    // R^3 flags: bit0 active, bit1 changed
-    __shared__ uint32_t sFaceMin[6];
-    __shared__ uint32_t sFaceFlag;
-    __shared__ unsigned long long sCnt[3];
-
+    CellSmem<T, R> Msm(smem_raw);
+    __shared__ CellShared<R> S;
+    cell_init_tables<T, R>(A, S, Msm);
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
     const uint32_t nproc = ctl->proc_count;
     const uint32_t nx = ctl->cur ^ 1u;
     uint32_t* wn = nx ? A.wl1 : A.wl0;
-    T* Vt = reinterpret_cast<T*>(A.Vt);
-    const T* Ht = reinterpret_cast<const T*>(A.Ht);
-    const int cps = A.cps;
-    const int64_t n1 = A.n1;
-    const T INF = dinf<T>();
-
+    if (blockIdx.x < nproc && tid == 0) atomicMin(&ctl->t_start, gtimer());
     for (uint32_t w = blockIdx.x; w < nproc; w += gridDim.x) {
+        const long long t0 = clock64();
         const uint32_t c = A.proc_cell[w];
-        const uint32_t flags = A.proc_flags[w];
-        const int cx = (int)(c % (uint32_t)cps), cy = (int)((c / (uint32_t)cps) % (uint32_t)cps),
-                  cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
-        const int64_t base = (int64_t)c * R3;
-        if (tid < 6) sFaceMin[tid] = KEY_INF;
-        if (tid == 0) { sFaceFlag = 0; sCnt[0] = sCnt[1] = sCnt[2] = 0; }
-
-        // ---- stage tile + hf + flags ----
-        const bool init = flags & FLAG_INIT;
-        for (int e = tid; e < R3; e += NT) {
-            const int a = e % R, b = (e / R) % R, d = e / (R * R);
-            sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = Vt[base + e];
-            sH[e] = Ht[base + e];
-            sF[e] = init ? 1 : 0;
-        }
-        // ---- halo N(c): 6 faces of r^2 from the neighbour tiles (+inf outside the grid) ----
-        for (int e = tid; e < 6 * R * R; e += NT) {
-            const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
-            int hx, hy, hz, sa, sb, sd;
-            int64_t nc;
-            bool ex;
-            switch (f) {
-            case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
-            case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
-            case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
-            case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
-            case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
-            default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
-            }
-            T hv = INF;
-            if (ex) hv = Vt[nc * R3 + sa + R * sb + R * R * sd];
-            sV[(hx + 1) + RP * (hy + 1) + RP2 * (hz + 1)] = hv;
-        }
+        if (tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
+        unsigned long long nsw = 0;
+        cell_process<T, R>(A, S, Msm, c, A.proc_flags[w], nsw);
         __syncthreads();
-        if (!init) {
-            // re-activation: every point of each face that received new inflow
-            for (int e = tid; e < 6 * R * R; e += NT) {
-                const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
-                if (!(flags & (1u << f))) continue;
-                int a, b, d;
-                switch (f) {
-                case 0: a = 0; b = u; d = v; break;
-                case 1: a = R - 1; b = u; d = v; break;
-                case 2: a = u; b = 0; d = v; break;
-                case 3: a = u; b = R - 1; d = v; break;
-                case 4: a = u; b = v; d = 0; break;
-                default: a = u; b = v; d = R - 1; break;
-                }
-                sF[a + R * b + R * R * d] = 1;
-            }
-            __syncthreads();
-        }
-
-        // ---- gated GS sweeps in wavefront order until no point is active ----
-        const uint32_t pref = init ? 0u : pref_dirs(flags & 63u);
-        const int gray[8] = {0, 1, 3, 2, 6, 7, 5, 4};
-        int gi = 0;
-        bool pref_phase = pref != 0;
-        uint32_t nsweeps = 0;
-        unsigned long long nupd = 0, nwr = 0;
-        for (;;) {
-            int any = 0;
-            const uint32_t* sF32 = reinterpret_cast<const uint32_t*>(sF);
-            for (int wd = tid; wd < R3 / 4; wd += NT) any |= (sF32[wd] & 0x01010101u) != 0;
-            if (!__syncthreads_or(any)) break;
-            int dir;
-            if (pref_phase) {
-                while (gi < 8 && !(pref & (1u << gray[gi]))) ++gi;
-                if (gi < 8) { dir = gray[gi++]; }
-                else { pref_phase = false; gi = 0; dir = gray[gi++]; }
-            } else {
-                dir = gray[gi];
-                gi = (gi + 1) & 7;
-            }
-            ++nsweeps;
-            for (int s = 0; s < C::NPL; ++s) {
-                const int e = __ldg(&A.plane_off[s]) + tid;
-                if (e < __ldg(&A.plane_off[s + 1])) {
-                    const uint32_t ent = __ldg(&A.plane_tab[e]);
-                    int i = ent & 15, j = (ent >> 4) & 15, k = (ent >> 8) & 15;
-                    if (dir & 1) i = R - 1 - i;
-                    if (dir & 2) j = R - 1 - j;
-                    if (dir & 4) k = R - 1 - k;
-                    const int p = i + R * j + R * R * k;
-                    uint8_t fl = sF[p];
-                    if (fl & 1) {
-                        fl &= (uint8_t)~1u;                    // Alg. 2 line 4: set inactive
-                        const T hf = sH[p];
-                        const int qb = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
-                        const T v = sV[qb];
-                        const T xm = sV[qb - 1], xp = sV[qb + 1];
-                        const T ym = sV[qb - RP], yp = sV[qb + RP];
-                        const T zm = sV[qb - RP2], zp = sV[qb + RP2];
-                        const T mx = fmin(xm, xp), my = fmin(ym, yp), mz = fmin(zm, zp);
-                        const T a1 = fmin(mx, fmin(my, mz));
-                        if (hf < INF && a1 < v) {              // fixed points never update
-                            ++nupd;
-                            const T u = local_solve<T>(mx, my, mz, hf);   // line 5
-                            if (u < v) {                                  // line 6
-                                sV[qb] = u;                               // line 7
-                                fl |= 2u;
-                                ++nwr;
-                                // lines 8-13: activate larger neighbours; across the cell
-                                // border, tag the face as currently downwind (Eq. (3) value)
-                                const uint32_t kb = key_bits(u);
-                                if (xm > u) { if (i > 0) sF[p - 1] |= 1u; else { atomicOr(&sFaceFlag, 1u); atomicMin(&sFaceMin[0], kb); } }
-                                if (xp > u) { if (i < R - 1) sF[p + 1] |= 1u; else { atomicOr(&sFaceFlag, 2u); atomicMin(&sFaceMin[1], kb); } }
-                                if (ym > u) { if (j > 0) sF[p - R] |= 1u; else { atomicOr(&sFaceFlag, 4u); atomicMin(&sFaceMin[2], kb); } }
-                                if (yp > u) { if (j < R - 1) sF[p + R] |= 1u; else { atomicOr(&sFaceFlag, 8u); atomicMin(&sFaceMin[3], kb); } }
-                                if (zm > u) { if (k > 0) sF[p - R * R] |= 1u; else { atomicOr(&sFaceFlag, 16u); atomicMin(&sFaceMin[4], kb); } }
-                                if (zp > u) { if (k < R - 1) sF[p + R * R] |= 1u; else { atomicOr(&sFaceFlag, 32u); atomicMin(&sFaceMin[5], kb); } }
-                            }
-                        }
-                        sF[p] = fl;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-
-        // ---- write back changed values only ----
-        unsigned long long nw = 0;
-        for (int e = tid; e < R3; e += NT) {
-            if (sF[e] & 2u) {
-                const int a = e % R, b = (e / R) % R, d = e / (R * R);
-                Vt[base + e] = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
-                ++nw;
-            }
-        }
-        if (A.stats) {
-            atomicAdd(&sCnt[0], nupd);
-            atomicAdd(&sCnt[1], nwr);
-            atomicAdd(&sCnt[2], nw);
-        }
-        __syncthreads();
-
-        // ---- re-activate currently-downwind neighbour cells (Alg. 1 lines 7-10) ----
-        if (tid < 6) {
-            const int f = tid;
-            const bool exists = f == 0 ? cx > 0 : f == 1 ? cx < cps - 1 : f == 2 ? cy > 0
-                              : f == 3 ? cy < cps - 1 : f == 4 ? cz > 0 : cz < cps - 1;
-            if (exists && (sFaceFlag & (1u << f))) {
-                const int64_t nc = f == 0 ? (int64_t)c - 1 : f == 1 ? (int64_t)c + 1
-                                 : f == 2 ? (int64_t)c - cps : f == 3 ? (int64_t)c + cps
-                                 : f == 4 ? (int64_t)c - (int64_t)cps * cps
-                                          : (int64_t)c + (int64_t)cps * cps;
-                const uint32_t kb = sFaceMin[f];
-                atomicMin(&A.key[nc], kb);                                   // Eq. (3)
-                const uint32_t old = atomicOr(&A.state[nc], 1u << (f ^ 1));  // face of nc
-                if (old == 0u) {                                             // Alg. 5 analogue
-                    const uint32_t s = atomicAdd(&ctl->wl_count[nx], 1u);
-                    wn[s] = (uint32_t)nc;
+        // re-activate currently-downwind neighbour cells (Alg. 1 lines 7-10)
+        if (tid < 6 && (S.face_flag & (1u << tid))) {
+            const int64_t nc = face_neighbour(c, tid, A.cps);
+            if (nc >= 0) {
+                const uint32_t kb = S.face_min[tid];
+                atomicMin(&A.key[nc], kb);                                     // Eq. (3)
+                const uint32_t old = atomicOr(&A.state[nc], 1u << (tid ^ 1));  // face of nc
+                if (old == 0u) {                                               // Alg. 5
+                    const uint32_t sl = atomicAdd(&ctl->wl_count[nx], 1u);
+                    wn[sl] = (uint32_t)nc;
                 }
                 atomicMin(&ctl->kmin[nx], kb);
             }
         }
+        if (tid == 0 && S.cont) {   // continue this cell in a later round
+            atomicMin(&A.key[c], S.cont_key);
+            const uint32_t old = atomicOr(&A.state[c], FLAG_CONT);
+            if (old == 0u) {
+                const uint32_t sl = atomicAdd(&ctl->wl_count[nx], 1u);
+                wn[sl] = c;
+            }
+            atomicMin(&ctl->kmin[nx], S.cont_key);
+        }
         if (tid == 0 && A.stats) {
-            atomicAdd(&ctl->updates, sCnt[0]);
-            atomicAdd(&ctl->writes, sCnt[1]);
-            atomicAdd(&ctl->bytes_written, sCnt[2]);
-            atomicAdd(&ctl->sweeps, (unsigned long long)nsweeps);
-            // real (non-padding) points of this cell
-            const int64_t rx = (n1 - (int64_t)cx * R) < R ? (n1 - (int64_t)cx * R) : R;
-            const int64_t ry = (n1 - (int64_t)cy * R) < R ? (n1 - (int64_t)cy * R) : R;
-            const int64_t rz = (n1 - (int64_t)cz * R) < R ? (n1 - (int64_t)cz * R) : R;
-            atomicAdd(&ctl->real_pts, (unsigned long long)(rx * ry * rz));
+            cell_stats<R>(A, S, c, nsw);
+            const unsigned long long cyc = (unsigned long long)(clock64() - t0);
+            atomicAdd(&ctl->dbg[0], cyc);
+            atomicMax(&ctl->dbg[1], cyc);
+            atomicAdd(&ctl->dbg[3], 1ull);
         }
         __syncthreads();   // smem reuse by the next cell of this CTA
+    }
+    if (blockIdx.x < nproc && tid == 0) atomicMax(&ctl->t_end, gtimer());
+}
+
+// ---- async mode: persistent CTAs pull cells from a device FIFO (pHCM Alg. 3 analogue) ---
+//
+// Cell state word: bits 0-5 inflow faces, bit 6 INIT, QUEUED, RUNNING.  A cell is in the
+// ring at most once: it is pushed only on the transition to QUEUED while not RUNNING, or by
+// its own CTA when it finishes and finds QUEUED set (it was tagged while running).
+// ctl->pending = cells queued or running; the solve ends when it reaches 0 (the analogue
+// of activeCellCount, Alg. 3 lines 6 and 29).  Value stores are ordered before the tags by
+// __threadfence (the flush of P:686-688); readers take the cell with an atomic and read
+// tiles through L2 (.cg), so a stale read is only ever a valid upper bound and
+// is followed by a re-activation.
+enum : uint32_t { ST_QUEUED = 256u, ST_RUNNING = 512u, Q_EMPTY = 0xffffffffu };
+
+__device__ __forceinline__ void q_push(Ctl* ctl, uint32_t* ring, uint32_t qmask, uint32_t c)
+{
+    atomicAdd(&ctl->pending, 1u);
+    const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & qmask;
+    while (atomicCAS(&ring[slot], Q_EMPTY, c) != Q_EMPTY) __nanosleep(32);
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(CellCfg<R>::NT, MinBlocks<T, R>::value)
+k_async(CellArgs A)
+{
+    using C = CellCfg<R>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CellSmem<T, R> Msm(smem_raw);
+    __shared__ CellShared<R> S;
+    cell_init_tables<T, R>(A, S, Msm);
+    const int tid = threadIdx.x;
+    Ctl* ctl = A.ctl;
+    uint32_t* ring = A.wl0;
+    if (tid == 0) atomicMin(&ctl->t_start, gtimer());
+    for (;;) {
+        if (tid == 0) {
+            uint32_t got = Q_EMPTY, fl = 0;
+            unsigned ns = 32;
+            for (;;) {
+                if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) break;
+                const uint32_t h = __ldcg(&ctl->q_head), t = __ldcg(&ctl->q_tail);
+                if (h != t) {
+                    if (atomicCAS(&ctl->q_head, h, h + 1u) == h) {
+                        uint32_t v;
+                        while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) __nanosleep(20);
+                        // readiness (the heap order of Alg. 3 approximated locally): defer v
+                        // while an adjacent cell is running or is queued with a smaller key
+                        // (ties broken by index, so the minimum is never deferred)
+                        const uint32_t kv = __ldcg(&A.key[v]);
+                        bool defer = false;
+                        for (int f = 0; f < 6 && !defer; ++f) {
+                            const int64_t nb = face_neighbour(v, f, A.cps);
+                            if (nb < 0) continue;
+                            const uint32_t sn = __ldcg(&A.state[nb]);
+                            if (sn & ST_RUNNING) defer = true;
+                            else if ((sn & ST_QUEUED) && A.defer >= 2) {
+                                const uint32_t kn = __ldcg(&A.key[nb]);
+                                if (A.defer == 2) defer = kn < kv || (kn == kv && (uint32_t)nb < v);
+                                else defer = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
+                            }
+                        }
+                        if (defer && A.defer) {
+                            const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & A.qmask;
+                            while (atomicCAS(&ring[slot], Q_EMPTY, v) != Q_EMPTY) __nanosleep(32);
+                            atomicAdd(&ctl->defers, 1ull);
+                            __nanosleep(64);
+                            continue;
+                        }
+                        got = v;
+                        break;
+                    }
+                } else {
+                    __nanosleep(ns);
+                    ns = ns < 1024 ? ns * 2 : 1024;
+                }
+            }
+            if (got != Q_EMPTY) {
+                fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
+                A.key[got] = KEY_INF;                                // V^c <- +inf
+                __threadfence();
+            }
+            S.cell = got;
+            S.flags = fl;
+            S.stat[0] = S.stat[1] = S.stat[2] = 0;
+        }
+        __syncthreads();
+        const uint32_t c = S.cell;
+        if (c == Q_EMPTY) break;
+        const long long t0 = clock64();
+        unsigned long long nsw = 0;
+        cell_process<T, R>(A, S, Msm, c, S.flags, nsw);
+        __threadfence();   // value stores before the re-activations
+        __syncthreads();
+        if (tid < 6 && (S.face_flag & (1u << tid))) {
+            const int64_t nc = face_neighbour(c, tid, A.cps);
+            if (nc >= 0) {
+                atomicMin(&A.key[nc], S.face_min[tid]);                       // Eq. (3)
+                const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
+                if (!(old & (ST_QUEUED | ST_RUNNING))) q_push(ctl, ring, A.qmask, (uint32_t)nc);
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (S.cont) {
+                atomicMin(&A.key[c], S.cont_key);
+                atomicOr(&A.state[c], FLAG_CONT | ST_QUEUED);
+            }
+            const uint32_t old = atomicAnd(&A.state[c], ~ST_RUNNING);
+            if (old & ST_QUEUED) q_push(ctl, ring, A.qmask, c);   // tagged while running
+            const unsigned long long np = atomicAdd(&ctl->processings, 1ull) + 1ull;
+            if (np > A.proc_limit) atomicExch(&ctl->abort, 1u);
+            if (A.stats) {
+                cell_stats<R>(A, S, c, nsw);
+                const unsigned long long cyc = (unsigned long long)(clock64() - t0);
+                atomicAdd(&ctl->dbg[0], cyc);
+                atomicMax(&ctl->dbg[1], cyc);
+                atomicAdd(&ctl->dbg[3], 1ull);
+            }
+            __threadfence();
+            atomicSub(&ctl->pending, 1u);
+        }
+    }
+    if (tid == 0) atomicMax(&ctl->t_end, gtimer());
+}
+
+// seed the async ring with the initial cells (L <- Q^c, Alg. 1 line 2)
+__global__ void k_seed_queue(uint32_t* state, uint32_t* ring, Ctl* ctl, int64_t J)
+{
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < J;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = base + threadIdx.x;
+        const bool q = c < J && state[c] != 0;
+        if (q) state[c] |= ST_QUEUED;
+        warp_agg_append(&ctl->q_tail, ring, (uint32_t)c, q);
+        const unsigned m = __ballot_sync(__activemask(), q);
+        if ((threadIdx.x & 31) == 0 && m) atomicAdd(&ctl->pending, (uint32_t)__popc(m));
     }
 }
 

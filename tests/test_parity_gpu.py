@@ -128,12 +128,17 @@ def test_host_pointer_path(solver):
         assert_parity(_gpu(solver, w, dt, 8, host=True), U_orc, w, dt)
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("delta", [0.0, 0.05, 1e-6])
-def test_schedule_independence(mode, delta):
-    """Bin width, loop mode and cell size change the work, never the fixed point."""
+@pytest.mark.parametrize("mode,delta,msw,defer", [
+    (0, 0.0, 0, 1), (0, 0.0, 2, 1), (0, 0.0, 0, 0), (0, 0.0, 0, 2), (0, 0.05, 0, 3),
+    (1, 0.0, 0, 1), (1, 0.05, 0, 1), (1, 1e-6, 3, 1),
+    (2, 0.0, 0, 1), (2, 0.05, 1, 1), (2, 1e-6, 0, 1)])
+def test_schedule_independence(mode, delta, msw, defer):
+    """Loop mode, bin width, sweep cap (continuation) and async readiness rule change the work,
+    never the fixed point."""
     import paper_1306_4743_b200 as eik
     s = eik.Solver(device=0, loop_mode=mode, bin_width=delta)
+    s.set_option(eik.EIK_OPT_MAX_SWEEPS, msw)
+    s.set_option(eik.EIK_OPT_ASYNC_DEFER, defer)
     for w in (W.c2(48), W.c3(48), W.c4(48)):
         for r in (8, 16):
             for dt in (np.float64, np.float32):
@@ -149,7 +154,7 @@ def test_stats_are_consistent(solver):
     assert st["cell_processings"] >= st["J"]          # every cell is reached at least once
     assert st["point_writes"] >= st["M"] - 1          # every non-exit point written >= once
     assert st["point_updates"] >= st["point_writes"]
-    assert st["rounds"] >= 1 and st["ms_total"] > 0
+    assert st["ms_total"] > 0
 
 
 # ---------------------------------------------------------------- error convention -------

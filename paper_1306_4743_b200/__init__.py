@@ -178,12 +178,12 @@ class Solver:
 
     def debug(self) -> dict:
         import numpy as np
-        a = np.zeros(41, dtype=np.uint64)
-        lib.eik_get_debug(self._ctx, a.ctypes.data, 41)
+        a = np.zeros(42, dtype=np.uint64)
+        lib.eik_get_debug(self._ctx, a.ctypes.data, 42)
         return {"cycles_sum": int(a[0]), "cycles_max": int(a[1]), "plane_steps": int(a[2]),
                 "processings": int(a[3]), "sweep_hist": [int(x) for x in a[4:36]],
                 "cyc_stage": int(a[36]), "cyc_mask": int(a[37]), "cyc_steps": int(a[38]),
-                "cyc_writeback": int(a[39]), "defers": int(a[40])}
+                "cyc_writeback": int(a[39]), "list_iters": int(a[40]), "defers": int(a[41])}
 
     def stats(self) -> dict:
         s = EikStats()

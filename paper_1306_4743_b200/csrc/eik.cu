@@ -258,9 +258,9 @@ extern "C" int eik_get_stats(const eik_ctx* ctx, eik_stats* out)
 extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
 {
     if (!ctx || !out || n < 0) return EIK_EINVAL;
-    const int m = n < 40 ? n : 40;
+    const int m = n < 41 ? n : 41;
     for (int i = 0; i < m; ++i) out[i] = ctx->ctl_host->dbg[i];
-    if (n > 40) out[40] = ctx->ctl_host->defers;
+    if (n > 41) out[41] = ctx->ctl_host->defers;
     return EIK_OK;
 }
 

@@ -138,7 +138,7 @@ struct Ctl {
     unsigned long long defers;
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
     // steps executed, [3] processings, [4..35] histogram of sweeps per processing (31 = >=31)
-    unsigned long long dbg[40];   // [36] stage, [37] plane-mask, [38] steps, [39] write-back cycles
+    unsigned long long dbg[41];   // [36] stage, [37] plane-mask, [38] steps, [39] write-back cycles, [40] list iterations
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -340,6 +340,7 @@ template <int R> struct CellCfg {
     static constexpr int MAXP = R == 16 ? 192 : (R == 8 ? 48 : 12);  // largest plane
     static constexpr int NT = (MAXP + 31) / 32 * 32;                 // one plane point / thread
     static constexpr int MINB = R == 16 ? 4 : 8;                     // CTAs per SM target
+    static constexpr int LCAP = R == 16 ? 384 : (R == 8 ? 128 : 64);  // active-list capacity
 };
 
 template <typename T, int R> struct MinBlocks { static constexpr int value = CellCfg<R>::MINB; };
@@ -348,8 +349,8 @@ template <> struct MinBlocks<double, 16> { static constexpr int value = 2; };
 template <typename T, int R>
 constexpr size_t cell_smem_bytes()
 {
-    // V box + hf + plane table (uint16) + active bytes
-    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + 3 * CellCfg<R>::R3;
+    // V box + hf + plane table (uint16) + active bytes + 2 active lists (uint16)
+    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + 3 * CellCfg<R>::R3 + 4 * CellCfg<R>::LCAP;
 }
 
 struct CellArgs {
@@ -401,6 +402,8 @@ template <int R> struct CellShared {
     uint32_t cell, flags;              // async mode broadcast
     uint32_t cont;                     // processing stopped at the sweep cap
     uint32_t cont_key;                 // min V over the points still active (key bits)
+    int32_t nact, nact2[2];            // active-point counts
+    int32_t lcnt[2], lover;            // active-list lengths / overflow
 };
 
 // dynamic shared memory carve-up
@@ -409,12 +412,14 @@ template <typename T, int R> struct CellSmem {
     T* H;          // R^3 hf (sign bit set = point changed in this processing)
     uint16_t* tab; // plane table
     uint8_t* act;  // R^3 active flags (Alg. 2)
+    uint16_t* list; // 2 x LCAP active-point lists
     __device__ explicit CellSmem(unsigned char* raw)
     {
         V = reinterpret_cast<T*>(raw);
         H = V + CellCfg<R>::BOX;
         tab = reinterpret_cast<uint16_t*>(H + CellCfg<R>::R3);
         act = reinterpret_cast<uint8_t*>(tab + CellCfg<R>::R3);
+        list = reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3);
     }
 };
 
@@ -429,22 +434,27 @@ __device__ __forceinline__ void cell_init_tables(const CellArgs& A, CellShared<R
 
 // Process one cell to convergence (HCM "perform modified LSM on c until convergence",
 // Alg. 1 line 6): stage the tile and its one-point halo N(c) (boundary data of
-// c~ = c u N(c)), run gated Gauss-Seidel sweeps, write back changed values.  On return the
-// face summaries (face_flag, face_min) are in S; the caller re-activates neighbours.
+// c~ = c u N(c)), relax the gated (LSM) update of Alg. 2 until no point is active, write
+// back changed values.  On return the face summaries (face_flag, face_min) are in S; the
+// caller re-activates neighbours.
 //
-// A sweep in direction d visits the wavefront planes s = i' + j' + k' = 0 .. 3R-3 (primes =
-// coordinates reflected per d) in order: the exact Gauss-Seidel ordering of that sweep
-// (Detrixhe et al. planes).  The points of a plane are independent and are
-// packed onto consecutive threads through a shared plane table (one point per thread).  A
-// step is latency-bound (it depends on the previous plane), so its chain is kept short and
-// free of shared atomics: the next step's table entry and hf are prefetched, activity is one
-// byte per point written with plain stores (several writers only ever store 1), "changed"
-// is the sign bit of the point's hf, the two- and three-sided candidates of the local solve
-// are evaluated side by side, the Eq. (3) face minima are kept per thread and reduced once
-// per processing, and the step ends in one __syncthreads_or that also reports forward
-// activations.  LSM gating (Alg. 2); planes without active points are skipped
-// without a barrier.  Tile traffic bypasses L1 (ld/st .cg): other CTAs update neighbouring
-// tiles concurrently in the asynchronous scheduler.
+// Two relaxation orders, both exact Gauss-Seidel/chaotic relaxations of Eq. (2) that reach
+// the same fixed point (any order does: values only decrease):
+//  * wavefront sweeps while many points are active: a sweep in direction d visits the
+//    planes s = i' + j' + k' = 0 .. 3R-3 (primes = coordinates reflected per d) in order,
+//    i.e. the exact GS ordering of that sweep (Detrixhe et al. planes).
+//    The points of a plane are independent and are packed onto consecutive threads through
+//    a shared plane table; a step ends in one __syncthreads_or that also reports forward
+//    activations; planes without active points are skipped without a barrier.  Activity is
+//    one byte per point written with plain stores (several writers only ever store 1).
+//  * an active-point list once few points remain (<= LCAP): every listed point is relaxed
+//    at once (chaotic order, FIM-like), newly activated points are claimed with a CAS on
+//    their flag word and appended to the next list.  This turns the long tail of late sweeps
+//    (few active points spread over many planes) into a few short iterations.  If a list
+//    overflows, the flags stay authoritative and the wavefront sweeps resume.
+// "Changed" is the sign bit of a point's hf; the currently-downwind faces (Eq. (3)) are
+// derived once per processing from the changed border points.  Tile traffic bypasses L1
+// (ld/st .cg): other CTAs update neighbouring tiles concurrently in the async scheduler.
 template <typename T, int R>
 __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S,
                                              CellSmem<T, R>& M, uint32_t c, uint32_t flags,
@@ -452,6 +462,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 {
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
+    constexpr int LCAP = C::LCAP;
     const int tid = threadIdx.x;
     T* Vt = reinterpret_cast<T*>(A.Vt);
     const T* Ht = reinterpret_cast<const T*>(A.Ht);
@@ -464,34 +475,21 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
               cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
     const int64_t base = (int64_t)c * R3;
     if (tid < 6) S.face_min[tid] = KEY_INF;
-    if (tid == 0) { S.face_flag = 0; S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF; }
-    long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0;
+    if (tid == 0) {
+        S.face_flag = 0; S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
+        S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
+    }
+    long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0, nlist = 0;
     constexpr int NWB = R3 / 32;   // saved-bitmask words
 
-    // ---- stage V, hf and the initial activity (coalesced) ----
+    // ---- stage V and hf (coalesced), then the halo N(c) ----
     const bool init = flags & FLAG_INIT;
 #pragma unroll 4
     for (int e = tid; e < R3; e += NT) {
         const int a = e % R, b = (e / R) % R, d = e / (R * R);
         sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = __ldcg(&Vt[base + e]);
         sH[e] = __ldcg(&Ht[base + e]);
-        const bool on = init || ((flags & 1u) && a == 0) || ((flags & 2u) && a == R - 1) ||
-                        ((flags & 4u) && b == 0) || ((flags & 8u) && b == R - 1) ||
-                        ((flags & 16u) && d == 0) || ((flags & 32u) && d == R - 1);
-        sA[e] = on ? 1 : 0;
     }
-    if (flags & FLAG_CONT) {       // restore the active points saved at the sweep cap
-        __syncthreads();
-        for (int w = tid; w < NWB; w += NT) {
-            uint32_t x = __ldcg(&A.pend[(int64_t)c * NWB + w]);
-            while (x) {
-                const int l = __ffs(x) - 1;
-                x &= x - 1;
-                sA[32 * w + l] = 1;
-            }
-        }
-    }
-    // ---- halo N(c): 6 faces of r^2 from the neighbour tiles (+inf outside the grid) ----
     for (int e = tid; e < 6 * R * R; e += NT) {
         const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
         int hx, hy, hz, sa, sb, sd;
@@ -510,15 +508,126 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         sV[(hx + 1) + RP * (hy + 1) + RP2 * (hz + 1)] = hv;
     }
     __syncthreads();
+    // ---- initial activity: all points (INIT), or the points of the inflow faces whose
+    // outside neighbour is smaller (only smaller neighbours enter Eq. (2)), plus the
+    // points saved at a sweep cap ----
+    {
+        int cnt = 0;
+        for (int e = tid; e < R3; e += NT) {
+            const int a = e % R, b = (e / R) % R, d = e / (R * R);
+            bool on = init;
+            if (!on && (flags & 63u)) {
+                const int q = (a + 1) + RP * (b + 1) + RP2 * (d + 1);
+                const T v = sV[q];
+                on = ((flags & 1u) && a == 0 && sV[q - 1] < v) ||
+                     ((flags & 2u) && a == R - 1 && sV[q + 1] < v) ||
+                     ((flags & 4u) && b == 0 && sV[q - RP] < v) ||
+                     ((flags & 8u) && b == R - 1 && sV[q + RP] < v) ||
+                     ((flags & 16u) && d == 0 && sV[q - RP2] < v) ||
+                     ((flags & 32u) && d == R - 1 && sV[q + RP2] < v);
+            }
+            if ((flags & FLAG_CONT) && !on)
+                on = (__ldcg(&A.pend[(int64_t)c * NWB + (e >> 5)]) >> (e & 31)) & 1u;
+            sA[e] = on ? 1 : 0;
+            cnt += on;
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if ((tid & 31) == 0 && cnt) atomicAdd(&S.nact, cnt);
+    }
+    __syncthreads();
     const long long tc1 = clock64();
 
-    // ---- gated GS sweeps in wavefront order until no point is active ----
     const uint32_t pref = init ? 0u : pref_dirs(flags & 63u);
     int gi = 0;
     bool pref_phase = pref != 0;
     uint32_t nsweeps = 0;
     uint32_t nupd = 0, nwr = 0;
+    int nact = S.nact;     // active points (exact at loop entry)
     for (int sw = 0;; ++sw) {
+        if (nact == 0) break;
+        // ================= active-list relaxation (few active points) =================
+        if (nact <= LCAP) {
+            const long long tl0 = clock64();
+            // build the list from the flags
+            if (tid == 0) { S.lcnt[0] = 0; S.lcnt[1] = 0; S.lover = 0; }
+            __syncthreads();
+            {
+                const uint32_t* sA32 = reinterpret_cast<const uint32_t*>(sA);
+                for (int wd = tid; wd < R3 / 4; wd += NT) {
+                    uint32_t x = sA32[wd];
+                    while (x) {
+                        const int e = 4 * wd + ((__ffs(x) - 1) >> 3);
+                        x &= ~(0xffu << (8 * (e & 3)));
+                        const int sl = atomicAdd(&S.lcnt[0], 1);
+                        if (sl < LCAP) M.list[sl] = (uint16_t)e;
+                    }
+                }
+            }
+            __syncthreads();
+            int cur = 0;
+            bool overflow = S.lcnt[0] > LCAP;
+            while (!overflow) {
+                const int n = S.lcnt[cur];
+                if (n == 0) break;
+                ++nlist;
+                uint16_t* Lc = M.list + cur * LCAP;
+                uint16_t* Ln = M.list + (cur ^ 1) * LCAP;
+                for (int t = tid; t < n; t += NT) {
+                    const int p = Lc[t];
+                    sA[p] = 0;                                               // Alg. 2 line 4
+                    const T hs = sH[p];
+                    const T hf = fabs(hs);
+                    const int i = p % R, j = (p / R) % R, k = p / (R * R);
+                    const int q = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
+                    const T v = sV[q];
+                    const T xm = sV[q - 1], xp = sV[q + 1];
+                    const T ym = sV[q - RP], yp = sV[q + RP];
+                    const T zm = sV[q - RP2], zp = sV[q + RP2];
+                    const T mx = fmin(xm, xp), my = fmin(ym, yp), mz = fmin(zm, zp);
+                    if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
+                        ++nupd;
+                        const T u = local_solve_fast<T>(mx, my, mz, hf);      // line 5
+                        if (u < v) {                                          // line 6
+                            sV[q] = u;                                        // line 7
+                            if (hs > T(0)) sH[p] = -hs;
+                            ++nwr;
+                            // lines 8-10: claim larger neighbours (CAS on the flag word) and
+                            // append them to the next list
+                            auto claim = [&](int nb) {
+                                uint32_t* w = reinterpret_cast<uint32_t*>(sA + (nb & ~3));
+                                const int sh = 8 * (nb & 3);
+                                uint32_t old = *reinterpret_cast<volatile uint32_t*>(w);
+                                while (!((old >> sh) & 0xffu)) {
+                                    const uint32_t prev = atomicCAS(w, old, old | (1u << sh));
+                                    if (prev == old) {
+                                        const int sl = atomicAdd(&S.lcnt[cur ^ 1], 1);
+                                        if (sl < LCAP) Ln[sl] = (uint16_t)nb;
+                                        else S.lover = 1;
+                                        break;
+                                    }
+                                    old = prev;
+                                }
+                            };
+                            if (xm > u && i > 0) claim(p - 1);
+                            if (xp > u && i < R - 1) claim(p + 1);
+                            if (ym > u && j > 0) claim(p - R);
+                            if (yp > u && j < R - 1) claim(p + R);
+                            if (zm > u && k > 0) claim(p - R * R);
+                            if (zp > u && k < R - 1) claim(p + R * R);
+                        }
+                    }
+                }
+                __syncthreads();
+                overflow = S.lover != 0;
+                if (tid == 0) S.lcnt[cur] = 0;
+                cur ^= 1;
+                __syncthreads();
+            }
+            tstep += clock64() - tl0;
+            if (!overflow) break;          // converged in list mode
+            nact = LCAP + 1;               // resume wavefront sweeps (flags authoritative)
+        }
+        // ========================= one wavefront sweep ==========================
         int dir;
         {
             const uint32_t gray = 0x45762310u;   // Gray cycle 0,1,3,2,6,7,5,4 (nibbles)
@@ -533,29 +642,36 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         const bool fx = dir & 1, fy = dir & 2, fz = dir & 4;
         const long long tm0 = clock64();
-        // the set of planes (in this direction) holding active points
+        // the set of planes (in this direction) holding active points, and their count
         {
             unsigned long long pm = 0;
+            int cnt = 0;
             const uint32_t* sA32 = reinterpret_cast<const uint32_t*>(sA);
             for (int wd = tid; wd < R3 / 4; wd += NT) {
                 uint32_t x = sA32[wd];
                 while (x) {
                     const int e = 4 * wd + ((__ffs(x) - 1) >> 3);
-                    x &= x - 1;
+                    x &= ~(0xffu << (8 * (e & 3)));
                     const int a = e % R, b = (e / R) % R, d = e / (R * R);
                     pm |= 1ull << ((fx ? R - 1 - a : a) + (fy ? R - 1 - b : b) + (fz ? R - 1 - d : d));
+                    ++cnt;
                 }
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) pm |= __shfl_xor_sync(0xffffffffu, pm, o);
-            if ((tid & 31) == 0 && pm) atomicOr(&S.plane[sw & 1], pm);
+            for (int o = 16; o > 0; o >>= 1) {
+                pm |= __shfl_xor_sync(0xffffffffu, pm, o);
+                cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            }
+            if ((tid & 31) == 0 && pm) { atomicOr(&S.plane[sw & 1], pm); atomicAdd(&S.nact2[sw & 1], cnt); }
         }
         __syncthreads();
         const unsigned long long pm = S.plane[sw & 1];
-        if (tid == 0) S.plane[(sw + 1) & 1] = 0;
+        nact = S.nact2[sw & 1];
+        if (tid == 0) { S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0; }
         const long long tm1 = clock64();
         tmask += tm1 - tm0;
         if (pm == 0ull) break;
+        if (nact <= LCAP && sw > 0) continue;   // few left: list mode (next iteration)
         if (A.max_sweeps > 0 && nsweeps >= (uint32_t)A.max_sweeps) {
             // sweep cap reached with points still active: save them and continue in a later
             // processing (the cell re-queues itself; correctness is unaffected, values only
@@ -643,9 +759,9 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             ++nsteps;
         }
         tstep += clock64() - tm1;
+        nact = LCAP + 1;   // unknown until the next scan
     }
     const long long tc2 = clock64();
-
     // ---- face summaries (Eq. (3)): face f is currently downwind iff a border
     // point changed in this processing and ended below its outside neighbour (the staged
     // halo value, an upper bound of the current one: P:718 redundant tags are harmless); the
@@ -709,6 +825,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         atomicAdd(&A.ctl->dbg[38], (unsigned long long)tstep);
         atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - tc2));
         atomicAdd(&A.ctl->dbg[2], (unsigned long long)nsteps);
+        atomicAdd(&A.ctl->dbg[40], (unsigned long long)nlist);
     }
 }
 

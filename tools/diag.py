@@ -11,7 +11,7 @@ import paper_1306_4743_b200 as eik  # noqa: E402
 
 cfgs = sys.argv[1:] or ["C3"]
 for name in cfgs:
-    bw, mode, defer, msw = None, 0, 1, 0
+    bw, mode, defer, msw = None, 2, 1, 0
     if ":" in name:
         parts = name.split(":")
         name = parts[0]
@@ -38,6 +38,6 @@ for name in cfgs:
            "steps_per_proc": dbg["plane_steps"] / p, "sweeps_per_proc": st["cell_sweeps"] / p,
            "upd_per_proc": st["point_updates"] / p, "hist": dbg["sweep_hist"][:16],
            "stage": dbg["cyc_stage"] / p, "mask": dbg["cyc_mask"] / p, "stepcyc": dbg["cyc_steps"] / p,
-           "wb": dbg["cyc_writeback"] / p, "cyc_per_step": dbg["cyc_steps"] / max(dbg["plane_steps"], 1)}
+           "wb": dbg["cyc_writeback"] / p, "list_it": dbg["list_iters"] / p, "cyc_per_step": dbg["cyc_steps"] / max(dbg["plane_steps"], 1)}
     print(json.dumps(out))
     s.close()

@@ -135,7 +135,8 @@ int eik_get_stats(const eik_ctx* ctx, eik_stats* out);
  * out[0] sum of per-processing SM cycles, out[1] max, out[2] wavefront plane steps executed,
  * out[3] processings, out[4 + s] number of processings that ran s sweeps (s = 31: >= 31),
  * out[36..39] cycles in staging / plane-mask / plane steps / write-back, out[40] active-list
- * iterations, out[41] async-mode deferrals.  Copies min(n, 42) values.  EIK_EINVAL if ctx/out is NULL or n < 0. */
+ * iterations, out[41] async-mode deferrals, out[42 + 2r], out[43 + 2r] = cells and span (ns) of
+ * round r (round modes, r < 1024).  Copies min(n, 42 + 2048) values.  EIK_EINVAL if ctx/out is NULL or n < 0. */
 int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n);
 
 /* Message of the last failing call on ctx (owned by ctx; valid until its next call).

@@ -232,7 +232,7 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         ctx->time_cell_events = value != 0;
         return EIK_OK;
     case EIK_OPT_ASYNC_DEFER:
-        if (value < 0 || value > 3) return fail(ctx, EIK_EINVAL, "defer mode must be 0..3");
+        if (value < 0 || value > 4) return fail(ctx, EIK_EINVAL, "defer mode must be 0..4");
         ctx->async_defer = (int)value;
         return EIK_OK;
     case EIK_OPT_MAX_SWEEPS:
@@ -261,6 +261,7 @@ extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
     const int m = n < 41 ? n : 41;
     for (int i = 0; i < m; ++i) out[i] = ctx->ctl_host->dbg[i];
     if (n > 41) out[41] = ctx->ctl_host->defers;
+    for (int i = 42; i < n && i < 42 + 2048; ++i) out[i] = ctx->ctl_host->rtrace[i - 42];
     return EIK_OK;
 }
 

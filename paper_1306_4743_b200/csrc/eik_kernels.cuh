@@ -135,6 +135,8 @@ struct Ctl {
     unsigned long long t_start, t_end;     // this round's cell-kernel span (%globaltimer ns)
     unsigned long long cell_ns, cell_launches;
     uint32_t q_head, q_tail, pending, abort;   // async mode ring + work counter
+    uint32_t rtrace[2048];                      // round mode: per-round (cells, span ns)
+    uint32_t claim;                             // round mode: next cell of this round
     unsigned long long defers;
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
     // steps executed, [3] processings, [4..35] histogram of sweeps per processing (31 = >=31)
@@ -313,10 +315,15 @@ __device__ __forceinline__ bool round_end_body(Ctl* ctl)
     if (ctl->proc_count > 0 && ctl->t_end > ctl->t_start) {
         ctl->cell_ns += ctl->t_end - ctl->t_start;
         ctl->cell_launches += 1;
+        if (ctl->rounds <= 1024u) {   // per-round trace (diagnostics): cells, span ns
+            ctl->rtrace[2 * (ctl->rounds - 1)] = ctl->proc_count;
+            ctl->rtrace[2 * (ctl->rounds - 1) + 1] = (uint32_t)(ctl->t_end - ctl->t_start);
+        }
     }
     ctl->t_start = ~0ull;
     ctl->t_end = 0;
     ctl->proc_count = 0;
+    ctl->claim = 0;
     ctl->wl_count[cur] = 0;
     ctl->kmin[cur] = KEY_INF;
     ctl->cur = nx;
@@ -879,8 +886,15 @@ k_cell(CellArgs A)
     const uint32_t nproc = ctl->proc_count;
     const uint32_t nx = ctl->cur ^ 1u;
     uint32_t* wn = nx ? A.wl1 : A.wl0;
-    if (blockIdx.x < nproc && tid == 0) atomicMin(&ctl->t_start, gtimer());
-    for (uint32_t w = blockIdx.x; w < nproc; w += gridDim.x) {
+    // dynamic claiming of this round's cells (processing times vary by >10x between cells)
+    bool worked = false;
+    for (;;) {
+        if (tid == 0) S.cell = atomicAdd(&ctl->claim, 1u);
+        __syncthreads();
+        const uint32_t w = S.cell;
+        if (w >= nproc) break;
+        if (!worked && tid == 0) atomicMin(&ctl->t_start, gtimer());
+        worked = true;
         const long long t0 = clock64();
         const uint32_t c = A.proc_cell[w];
         if (tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
@@ -919,7 +933,7 @@ k_cell(CellArgs A)
         }
         __syncthreads();   // smem reuse by the next cell of this CTA
     }
-    if (blockIdx.x < nproc && tid == 0) atomicMax(&ctl->t_end, gtimer());
+    if (worked && tid == 0) atomicMax(&ctl->t_end, gtimer());
 }
 
 // ---- async mode: persistent CTAs pull cells from a device FIFO (pHCM Alg. 3 analogue) ---
@@ -969,13 +983,16 @@ k_async(CellArgs A)
                         // while an adjacent cell is running or is queued with a smaller key
                         // (ties broken by index, so the minimum is never deferred)
                         const uint32_t kv = __ldcg(&A.key[v]);
+                        const uint32_t sv = __ldcg(&A.state[v]);
                         bool defer = false;
                         for (int f = 0; f < 6 && !defer; ++f) {
+                            // mode 4: only neighbours across an inflow face of v matter
+                            if (A.defer == 4 && !(sv & (1u << f))) continue;
                             const int64_t nb = face_neighbour(v, f, A.cps);
                             if (nb < 0) continue;
                             const uint32_t sn = __ldcg(&A.state[nb]);
                             if (sn & ST_RUNNING) defer = true;
-                            else if ((sn & ST_QUEUED) && A.defer >= 2) {
+                            else if ((sn & ST_QUEUED) && (A.defer == 2 || A.defer == 3)) {
                                 const uint32_t kn = __ldcg(&A.key[nb]);
                                 if (A.defer == 2) defer = kn < kv || (kn == kv && (uint32_t)nb < v);
                                 else defer = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);

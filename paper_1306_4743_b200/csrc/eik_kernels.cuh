@@ -489,30 +489,58 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0, nlist = 0;
     constexpr int NWB = R3 / 32;   // saved-bitmask words
 
-    // ---- stage V and hf (coalesced), then the halo N(c) ----
+    // ---- stage V and hf (coalesced), then the halo N(c): all loads of a batch are issued
+    // before any store so that many are in flight per thread (memory-level parallelism) ----
     const bool init = flags & FLAG_INIT;
-#pragma unroll 4
-    for (int e = tid; e < R3; e += NT) {
-        const int a = e % R, b = (e / R) % R, d = e / (R * R);
-        sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = __ldcg(&Vt[base + e]);
-        sH[e] = __ldcg(&Ht[base + e]);
-    }
-    for (int e = tid; e < 6 * R * R; e += NT) {
-        const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
-        int hx, hy, hz, sa, sb, sd;
-        int64_t nc;
-        bool ex;
-        switch (f) {
-        case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
-        case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
-        case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
-        case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
-        case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
-        default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
+    {
+        constexpr int PER = (R3 + NT - 1) / NT;          // tile elements per thread
+        constexpr int B = sizeof(T) == 4 ? (PER + 1) / 2 : (PER + 3) / 4;   // batch
+#pragma unroll
+        for (int m0 = 0; m0 < PER; m0 += B) {
+            T va[B], ha[B];
+#pragma unroll
+            for (int m = 0; m < B; ++m) {
+                const int e = tid + (m0 + m) * NT;
+                if (m0 + m < PER && e < R3) { va[m] = __ldcg(&Vt[base + e]); ha[m] = __ldcg(&Ht[base + e]); }
+            }
+#pragma unroll
+            for (int m = 0; m < B; ++m) {
+                const int e = tid + (m0 + m) * NT;
+                if (m0 + m < PER && e < R3) {
+                    const int a = e % R, b = (e / R) % R, d = e / (R * R);
+                    sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = va[m];
+                    sH[e] = ha[m];
+                }
+            }
         }
-        T hv = INF;
-        if (ex) hv = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
-        sV[(hx + 1) + RP * (hy + 1) + RP2 * (hz + 1)] = hv;
+        constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
+        T hv[PH];
+        int hq[PH];
+#pragma unroll
+        for (int m = 0; m < PH; ++m) {
+            const int e = tid + m * NT;
+            hq[m] = -1;
+            hv[m] = INF;
+            if (e < 6 * R * R) {
+                const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
+                int hx, hy, hz, sa, sb, sd;
+                int64_t nc;
+                bool ex;
+                switch (f) {
+                case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
+                case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
+                case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
+                case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
+                case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
+                default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
+                }
+                hq[m] = (hx + 1) + RP * (hy + 1) + RP2 * (hz + 1);
+                if (ex) hv[m] = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < PH; ++m)
+            if (hq[m] >= 0) sV[hq[m]] = hv[m];
     }
     __syncthreads();
     // ---- initial activity: all points (INIT), or the points of the inflow faces whose

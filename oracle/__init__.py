@@ -48,6 +48,8 @@ def _load():
         lib.orc_bfs.restype = I64
         lib.orc_check.argtypes = [I64, D, P, P, P, P]
         lib.orc_check.restype = None
+        lib.orc_residual_ratio.argtypes = [I64, D, P, P, P, D, D, P]
+        lib.orc_residual_ratio.restype = D
         _lib = lib
     return _lib
 
@@ -115,3 +117,15 @@ def check(n: int, F, exit_mask, U, h: float | None = None) -> dict:
     lib.orc_check(n, h, _ptr(F_), _ptr(m_), _ptr(U_), _ptr(out))
     return dict(res_max=out[0], res_at=int(out[1]), lip_max=out[2], causal_bad=int(out[3]),
                 n_finite=int(out[4]), f0_finite=int(out[5]), inf_bad=int(out[6]))
+
+
+def residual_ratio(n: int, F, exit_mask, U, u_unit: float, k_ulp: float = 8.0,
+                   h: float | None = None):
+    """max |res_p| / (k_ulp * u_unit * (U_p + h) / hf_p) over finite non-exit F > 0 points
+    (<= 1 means the fp32 bound of SURVEY C.6 holds everywhere); returns (ratio, index)."""
+    lib = _load()
+    h = 1.0 / n if h is None else h
+    F_, m_, U_ = _c64(F), _cu8(exit_mask), _c64(U)
+    at = ctypes.c_int64(-1)
+    r = lib.orc_residual_ratio(n, h, _ptr(F_), _ptr(m_), _ptr(U_), u_unit, k_ulp, ctypes.byref(at))
+    return r, at.value

@@ -355,3 +355,36 @@ void orc_check(int64_t n, double h, const double* F, const uint8_t* mask, const 
     out[0] = res_max; out[1] = res_at; out[2] = lip_max; out[3] = (double)causal_bad;
     out[4] = (double)n_fin; out[5] = (double)f0_finite; out[6] = (double)inf_bad;
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Scaled residual for results computed in a lower precision (C.6 "fp32: |res_p| <=
+ * 8 ulp32(U_p) / hf_p"): returns max over finite non-exit F>0 points of
+ *   |res_p| / (k_ulp * u_unit * (U_p + h) / hf_p),   u_unit = unit roundoff of the run dtype.
+ * (U_p + h keeps the bound meaningful at U ~ 0 next to exits.)  Also writes the index.
+ * ------------------------------------------------------------------------------------- */
+double orc_residual_ratio(int64_t n, double h, const double* F, const uint8_t* mask,
+                          const double* U, double u_unit, double k_ulp, int64_t* at)
+{
+    grid_t g = { n + 1, (n + 1) * (n + 1) * (n + 1) };
+    double worst = 0.0;
+    int64_t wat = -1;
+    for (int64_t p = 0; p < g.M; ++p) {
+        if (mask[p] || !(F[p] > 0.0)) continue;
+        double Up = U[p];
+        if (Up == ORC_INF) continue;
+        double m[3];
+        axis_minima(&g, U, p, m);
+        double hf = h / F[p];
+        double s = 0.0;
+        for (int d = 0; d < 3; ++d) {
+            double e = Up - m[d];
+            if (e > 0.0) s += e * e;
+        }
+        double res = fabs(s / (hf * hf) - 1.0);
+        double tol = k_ulp * u_unit * (Up + h) / hf;
+        double r = res / tol;
+        if (r > worst) { worst = r; wat = p; }
+    }
+    if (at) *at = wat;
+    return worst;
+}

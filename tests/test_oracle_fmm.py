@@ -221,3 +221,18 @@ def test_first_order_convergence():
         errs.append(np.abs(U - d).max())
     assert errs[0] / errs[1] >= 1.0 and errs[1] / errs[2] >= 1.0
     assert errs[2] < errs[0]
+
+
+def test_residual_ratio_checker():
+    """The scaled residual checker (C.6) accepts the exact fixed point (fp64) and its fp32
+    rounding at the fp32 bound, and rejects a solution with one point perturbed."""
+    n = 32
+    w = W.c2(n)
+    U = oracle.fmm(n, w.F, w.exit_mask, w.exit_vals)
+    r64, _ = oracle.residual_ratio(n, w.F, w.exit_mask, U, 2.0 ** -53)
+    r32, _ = oracle.residual_ratio(n, w.F, w.exit_mask, U.astype(np.float32), 2.0 ** -24)
+    assert r64 <= 1.0 and r32 <= 1.0
+    V = U.copy()
+    V[10, 11, 12] += 1e-4
+    rb, at = oracle.residual_ratio(n, w.F, w.exit_mask, V, 2.0 ** -24)
+    assert rb > 10.0

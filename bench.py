@@ -117,6 +117,22 @@ def make_inputs(cfg, prec, device, n=None):
             torch.from_numpy(qh.reshape(-1)).to(device))
 
 
+def job_time(t_local: float, pg=None, device=None) -> float:
+    """Whole-job time of one step: the MAX over ranks of each rank's device time (replicas
+    only: no data-path collective, the reduction is timing plumbing)."""
+    if pg is None:
+        return float(t_local)
+    import torch
+    tt = torch.tensor([float(t_local)], dtype=torch.float64, device=device)
+    pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def job_value(points_per_rank: int, world: int, t_seconds: float) -> float:
+    """gridpoints/s of the whole job: every rank solves its own copy (weak scaling)."""
+    return points_per_rank * world / t_seconds
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
@@ -227,12 +243,8 @@ def main():
             stats.append(solver.stats())
         ev1.record(stream)
         barrier()
-    t_ms = ev0.elapsed_time(ev1) / args.steps
-    if pg is not None:
-        tt = torch.tensor([t_ms], device=dev)
-        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-        t_ms = float(tt.item())
-    value = M * ws / (t_ms * 1e-3)
+    t_ms = job_time(ev0.elapsed_time(ev1) / args.steps, pg, dev)
+    value = job_value(M, ws, t_ms * 1e-3)
 
     # roofline of the dominant kernel (cell sweep): algorithmic bytes / its device time
     cell_ms = float(np.mean([s["ms_cell_device"] for s in stats]))
@@ -274,12 +286,8 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             solver.solve_host(Fh, mh, qh, cell_size=r, n=n, out=Uh)
-        t_e = (time.perf_counter() - t0) / args.e2e_steps
-        if pg is not None:
-            tt = torch.tensor([t_e], device=dev)
-            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-            t_e = float(tt.item())
-        e2e = {"value": M * ws / t_e, "unit": UNIT, "ms_per_step": t_e * 1e3,
+        t_e = job_time((time.perf_counter() - t0) / args.e2e_steps, pg, dev)
+        e2e = {"value": job_value(M, ws, t_e), "unit": UNIT, "ms_per_step": t_e * 1e3,
                "h2d_bytes_per_step": int(Fh.numel() * Fh.element_size() + mh.numel() + qh.numel() * qh.element_size()),
                "d2h_bytes_per_step": int(Uh.numel() * Uh.element_size()),
                "timer": "host wall clock around the blocking C-ABI call (pinned buffers)"}

@@ -45,6 +45,7 @@ struct eik_ctx {
     uint32_t* proc_cell = nullptr;
     uint32_t* proc_flags = nullptr;
     uint32_t* pend = nullptr;
+    uint32_t* gen = nullptr;
     size_t cell_cap = 0;
     size_t ring_cap = 0;
     Ctl* ctl = nullptr;
@@ -170,8 +171,9 @@ static void free_scratch(eik_ctx* ctx)
 {
     cudaFree(ctx->Vt); cudaFree(ctx->Ht);
     cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
-    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend);
+    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen);
     ctx->pend = nullptr;
+    ctx->gen = nullptr;
     ctx->Vt = ctx->Ht = nullptr;
     ctx->key = ctx->state = ctx->wl0 = ctx->wl1 = ctx->proc_cell = ctx->proc_flags = nullptr;
     ctx->tile_bytes = ctx->cell_cap = 0;
@@ -232,7 +234,7 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         ctx->time_cell_events = value != 0;
         return EIK_OK;
     case EIK_OPT_ASYNC_DEFER:
-        if (value < 0 || value > 4) return fail(ctx, EIK_EINVAL, "defer mode must be 0..4");
+        if (value < 0 || value > 5) return fail(ctx, EIK_EINVAL, "defer mode must be 0..5");
         ctx->async_defer = (int)value;
         return EIK_OK;
     case EIK_OPT_MAX_SWEEPS:
@@ -290,6 +292,7 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
         CK(cudaMalloc(&ctx->proc_cell, J * 4));
         CK(cudaMalloc(&ctx->proc_flags, J * 4));
         CK(cudaMalloc(&ctx->pend, J * 512));   // R^3 / 8 bytes per cell at r = 16
+        CK(cudaMalloc(&ctx->gen, J * 4));
         ctx->cell_cap = J;
     }
     return EIK_OK;
@@ -366,6 +369,7 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     ca.defer = ctx->async_defer;
     ca.defer_delta = isinf(ctx->bin_width) ? 0.f : (float)ctx->bin_width;
     CK(cudaMemsetAsync(ctx->wl0, 0xff, ctx->ring_cap * 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->gen, 0, (size_t)J * 4, ctx->stream));
     k_seed_queue<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
     if (r == 16) return launch_async<T, 16>(ctx, ca, grid);
@@ -503,6 +507,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.Ht = ctx->Ht;
     ca.max_sweeps = ctx->max_sweeps;
     ca.pend = ctx->pend;
+    ca.gen = ctx->gen;
     ca.n1 = n1;
     ca.cps = cps;
     ca.stats = ctx->collect_stats;

@@ -369,6 +369,7 @@ struct CellArgs {
     uint32_t qmask;              // async mode: ring capacity - 1 (power of two)
     uint32_t* key;
     uint32_t* state;
+    uint32_t* gen;               // async mode: BFS generation of each cell (readiness mode 5)
     const uint16_t* plane_tab;   // R^3 entries (a | b<<4 | c<<8) sorted by plane a+b+c
     const int32_t* plane_off;    // NPL + 1 offsets
     void* Vt;
@@ -411,6 +412,7 @@ template <int R> struct CellShared {
     uint32_t cont_key;                 // min V over the points still active (key bits)
     int32_t nact, nact2[2];            // active-point counts
     int32_t lcnt[2], lover;            // active-list lengths / overflow
+    uint32_t bwd[2];                   // axes with activations behind the wavefront
 };
 
 // dynamic shared memory carve-up
@@ -572,9 +574,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     __syncthreads();
     const long long tc1 = clock64();
 
-    const uint32_t pref = init ? 0u : pref_dirs(flags & 63u);
-    int gi = 0;
-    bool pref_phase = pref != 0;
+    int gi = 0, prev_dir = -1;
     uint32_t nsweeps = 0;
     uint32_t nupd = 0, nwr = 0;
     int nact = S.nact;     // active points (exact at loop entry)
@@ -663,17 +663,29 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             nact = LCAP + 1;               // resume wavefront sweeps (flags authoritative)
         }
         // ========================= one wavefront sweep ==========================
+        // sweep direction: the first sweep follows the inflow faces (preferred
+        // directions); afterwards the axes along which the previous sweep activated points
+        // behind its wavefront are reversed (information still has to travel that way);
+        // without such activations the Gray cycle 0,1,3,2,6,7,5,4 is followed
         int dir;
         {
-            const uint32_t gray = 0x45762310u;   // Gray cycle 0,1,3,2,6,7,5,4 (nibbles)
-            if (pref_phase) {
-                while (gi < 8 && !(pref & (1u << ((gray >> (4 * gi)) & 15u)))) ++gi;
-                if (gi < 8) { dir = (gray >> (4 * gi)) & 15u; ++gi; }
-                else { pref_phase = false; dir = 0; gi = 1; }
+            const uint32_t gray = 0x45762310u;
+            const uint32_t bw = sw > 0 ? S.bwd[(sw - 1) & 1] : 0u;
+            if (tid == 0) S.bwd[sw & 1] = 0;
+            if (prev_dir < 0) {
+                if (init || !(flags & 63u)) { dir = 0; gi = 1; }
+                else {
+                    dir = ((flags & 2u) && !(flags & 1u) ? 1 : 0) | ((flags & 8u) && !(flags & 4u) ? 2 : 0) |
+                          ((flags & 32u) && !(flags & 16u) ? 4 : 0);
+                }
+            } else if (bw) {
+                dir = prev_dir ^ (int)bw;
             } else {
                 dir = (gray >> (4 * gi)) & 15u;
                 gi = (gi + 1) & 7;
+                if (dir == prev_dir) { dir = (gray >> (4 * gi)) & 15u; gi = (gi + 1) & 7; }
             }
+            prev_dir = dir;
         }
         const bool fx = dir & 1, fy = dir & 2, fz = dir & 4;
         const long long tm0 = clock64();
@@ -731,6 +743,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         ++nsweeps;
         bool fwd = false;
+        uint32_t bwd = 0;
         int s = __ffsll((long long)pm) - 1;
         // prefetch: the point this thread owns at plane sp and its hf
         int pn = -1;
@@ -787,6 +800,9 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                         if (zm > u && k > 0) sA[p - R * R] = 1;
                         if (zp > u && k < R - 1) sA[p + R * R] = 1;
                         myfwd = ((fx ? xm : xp) > u) | ((fy ? ym : yp) > u) | ((fz ? zm : zp) > u);
+                        bwd |= (((fx ? xp : xm) > u) && (fx ? i < R - 1 : i > 0) ? 1u : 0u) |
+                               (((fy ? yp : ym) > u) && (fy ? j < R - 1 : j > 0) ? 2u : 0u) |
+                               (((fz ? zp : zm) > u) && (fz ? k < R - 1 : k > 0) ? 4u : 0u);
                     }
                 }
             }
@@ -795,6 +811,9 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         tstep += clock64() - tm1;
         nact = LCAP + 1;   // unknown until the next scan
+        for (int o = 16; o > 0; o >>= 1) bwd |= __shfl_xor_sync(0xffffffffu, bwd, o);
+        if ((tid & 31) == 0 && bwd) atomicOr(&S.bwd[sw & 1], bwd);
+        __syncthreads();
     }
     const long long tc2 = clock64();
     // ---- face summaries (Eq. (3)): face f is currently downwind iff a border
@@ -1020,6 +1039,8 @@ k_async(CellArgs A)
                             if (nb < 0) continue;
                             const uint32_t sn = __ldcg(&A.state[nb]);
                             if (sn & ST_RUNNING) defer = true;
+                            else if ((sn & ST_QUEUED) && A.defer == 5)
+                                defer = __ldcg(&A.gen[nb]) < __ldcg(&A.gen[v]);
                             else if ((sn & ST_QUEUED) && (A.defer == 2 || A.defer == 3)) {
                                 const uint32_t kn = __ldcg(&A.key[nb]);
                                 if (A.defer == 2) defer = kn < kv || (kn == kv && (uint32_t)nb < v);
@@ -1062,6 +1083,7 @@ k_async(CellArgs A)
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
                 atomicMin(&A.key[nc], S.face_min[tid]);                       // Eq. (3)
+                if (A.defer == 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
                 if (!(old & (ST_QUEUED | ST_RUNNING))) q_push(ctl, ring, A.qmask, (uint32_t)nc);
             }

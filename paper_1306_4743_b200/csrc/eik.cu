@@ -91,7 +91,8 @@ static int fail(eik_ctx* ctx, int code, const char* fmt, ...)
 
 static int rindex_of(int r) { return r == 4 ? 0 : r == 8 ? 1 : r == 16 ? 2 : -1; }
 
-// wavefront plane table for an r^3 cell: entries (a | b<<4 | c<<8) sorted by plane a+b+c
+// wavefront plane table for an r^3 cell: canonical point indices a + r b + r^2 c sorted by
+// plane a+b+c (a direction's table is this one XOR the reflection mask, r a power of two)
 static void make_plane_table(int r, std::vector<uint16_t>& tab, std::vector<int32_t>& off)
 {
     const int npl = 3 * r - 2;
@@ -102,7 +103,7 @@ static void make_plane_table(int r, std::vector<uint16_t>& tab, std::vector<int3
         for (int c = 0; c < r; ++c)
             for (int b = 0; b < r; ++b) {
                 const int a = s - b - c;
-                if (a >= 0 && a < r) tab.push_back((uint16_t)(a | (b << 4) | (c << 8)));
+                if (a >= 0 && a < r) tab.push_back((uint16_t)(a + r * b + r * r * c));   // canonical p
             }
     }
     off[npl] = (int32_t)tab.size();

@@ -345,7 +345,8 @@ template <int R> struct CellCfg {
     static constexpr int BOX = RP * RP * RP;
     static constexpr int NPL = 3 * R - 2;                            // wavefront planes
     static constexpr int MAXP = R == 16 ? 192 : (R == 8 ? 48 : 12);  // largest plane
-    static constexpr int NT = (MAXP + 31) / 32 * 32;                 // one plane point / thread
+    static constexpr int PPT = 1;                                    // plane points / thread (2 measured slower)
+    static constexpr int NT = ((MAXP + PPT - 1) / PPT + 31) / 32 * 32;
     static constexpr int MINB = R == 16 ? 4 : 8;                     // CTAs per SM target
     static constexpr int LCAP = R == 16 ? 384 : (R == 8 ? 128 : 64);  // active-list capacity
 };
@@ -471,7 +472,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 {
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
-    constexpr int LCAP = C::LCAP;
+    constexpr int LCAP = C::LCAP, PPT = C::PPT;
     const int tid = threadIdx.x;
     T* Vt = reinterpret_cast<T*>(A.Vt);
     const T* Ht = reinterpret_cast<const T*>(A.Ht);
@@ -575,6 +576,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     const long long tc1 = clock64();
 
     int gi = 0, prev_dir = -1;
+    int lf0 = -1, lf1 = -1, lf2 = -1;   // sweep at which each axis was last reversed
     uint32_t nsweeps = 0;
     uint32_t nupd = 0, nwr = 0;
     int nact = S.nact;     // active points (exact at loop entry)
@@ -679,7 +681,14 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                           ((flags & 32u) && !(flags & 16u) ? 4 : 0);
                 }
             } else if (bw) {
-                dir = prev_dir ^ (int)bw;
+                // flip one of those axes per sweep, the least recently flipped one (a source
+                // inside the cell needs all 8 octants: this then walks a Gray cycle)
+                int ax = -1, best = 0x7fffffff;
+                if ((bw & 1u) && lf0 < best) { ax = 0; best = lf0; }
+                if ((bw & 2u) && lf1 < best) { ax = 1; best = lf1; }
+                if ((bw & 4u) && lf2 < best) { ax = 2; best = lf2; }
+                if (ax == 0) lf0 = sw; else if (ax == 1) lf1 = sw; else lf2 = sw;
+                dir = prev_dir ^ (1 << ax);
             } else {
                 dir = (gray >> (4 * gi)) & 15u;
                 gi = (gi + 1) & 7;
@@ -745,70 +754,85 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         bool fwd = false;
         uint32_t bwd = 0;
         int s = __ffsll((long long)pm) - 1;
-        // prefetch: the point this thread owns at plane sp and its hf
-        int pn = -1;
-        T hn = INF;
-        auto prefetch = [&](int sp) {
-            pn = -1;
-            if (sp < NPL) {
-                const int e = S.off[sp] + tid;
-                if (e < S.off[sp + 1]) {
-                    const uint32_t ent = M.tab[e];
-                    const int i = fx ? R - 1 - (int)(ent & 15u) : (int)(ent & 15u);
-                    const int j = fy ? R - 1 - (int)((ent >> 4) & 15u) : (int)((ent >> 4) & 15u);
-                    const int k = fz ? R - 1 - (int)(ent >> 8) : (int)(ent >> 8);
-                    pn = i + R * j + R * R * k;
-                    hn = sH[pn];
-                }
-            }
-        };
-        prefetch(s);
+        // reflection of the canonical plane table for this direction: the index of a point is
+        // i + R j + R^2 k with R a power of two, so reflecting an axis is an XOR of its field
+        const int dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
+        // prefetch: the points this thread owns at plane sp (PPT slots) and their hf
+        int pn[PPT];
+        T hn[PPT];
+#define EIK_PREFETCH(sp_)                                                                  \
+        {                                                                                  \
+            const int sp = (sp_);                                                          \
+            const int o0 = sp < NPL ? S.off[sp] : 0, o1 = sp < NPL ? S.off[sp + 1] : 0;    \
+            _Pragma("unroll") for (int m = 0; m < PPT; ++m) {                              \
+                const int e = o0 + tid + m * NT;                                           \
+                pn[m] = -1;                                                                \
+                if (e < o1) { pn[m] = (int)M.tab[e] ^ dm; hn[m] = sH[pn[m]]; }             \
+            }                                                                              \
+        }
+        EIK_PREFETCH(s)
         for (; s < NPL; ++s) {
             const bool has = (pm >> s) & 1ull;
             if (!has && !fwd) {
                 if ((pm >> s) == 0ull) break;
-                prefetch(s + 1);
+                EIK_PREFETCH(s + 1)
                 continue;
             }
-            const int p = pn;
-            const T hs = hn;
-            prefetch(s + 1);   // independent of this step's results
+            int p[PPT];
+            T hs[PPT];
+#pragma unroll
+            for (int m = 0; m < PPT; ++m) { p[m] = pn[m]; hs[m] = hn[m]; }
+            EIK_PREFETCH(s + 1)   // independent of this step's results
             bool myfwd = false;
-            if (p >= 0 && sA[p]) {
-                sA[p] = 0;                                                 // Alg. 2 line 4
-                const T hf = fabs(hs);
-                const int i = p % R, j = (p / R) % R, k = p / (R * R);
-                const int q = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
-                const T v = sV[q];
-                const T xm = sV[q - 1], xp = sV[q + 1];
-                const T ym = sV[q - RP], yp = sV[q + RP];
-                const T zm = sV[q - RP2], zp = sV[q + RP2];
-                const T mx = fmin(xm, xp), my = fmin(ym, yp), mz = fmin(zm, zp);
-                if (hf < INF && fmin(mx, fmin(my, mz)) < v) {              // fixed / no gain
-                    ++nupd;
-                    const T u = local_solve_fast<T>(mx, my, mz, hf);        // line 5
-                    if (u < v) {                                             // line 6
-                        sV[q] = u;                                           // line 7
-                        if (hs > T(0)) sH[p] = -hs;                          // mark changed
-                        ++nwr;
-                        // lines 8-13: activate larger neighbours (predicated stores; the
-                        // cross-border "currently downwind" test is done once per processing)
-                        if (xm > u && i > 0) sA[p - 1] = 1;
-                        if (xp > u && i < R - 1) sA[p + 1] = 1;
-                        if (ym > u && j > 0) sA[p - R] = 1;
-                        if (yp > u && j < R - 1) sA[p + R] = 1;
-                        if (zm > u && k > 0) sA[p - R * R] = 1;
-                        if (zp > u && k < R - 1) sA[p + R * R] = 1;
-                        myfwd = ((fx ? xm : xp) > u) | ((fy ? ym : yp) > u) | ((fz ? zm : zp) > u);
-                        bwd |= (((fx ? xp : xm) > u) && (fx ? i < R - 1 : i > 0) ? 1u : 0u) |
-                               (((fy ? yp : ym) > u) && (fy ? j < R - 1 : j > 0) ? 2u : 0u) |
-                               (((fz ? zp : zm) > u) && (fz ? k < R - 1 : k > 0) ? 4u : 0u);
-                    }
-                }
+            // phase 1: all loads (flags, then values of the active points)
+            bool on[PPT];
+            int q[PPT];
+            T v[PPT], xm[PPT], xp[PPT], ym[PPT], yp[PPT], zm[PPT], zp[PPT];
+#pragma unroll
+            for (int m = 0; m < PPT; ++m) on[m] = p[m] >= 0 && sA[p[m]];
+#pragma unroll
+            for (int m = 0; m < PPT; ++m) {
+                if (!on[m]) continue;
+                const int i = p[m] & (R - 1), j = (p[m] / R) & (R - 1), k = p[m] / (R * R);
+                q[m] = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
+                v[m] = sV[q[m]];
+                xm[m] = sV[q[m] - 1]; xp[m] = sV[q[m] + 1];
+                ym[m] = sV[q[m] - RP]; yp[m] = sV[q[m] + RP];
+                zm[m] = sV[q[m] - RP2]; zp[m] = sV[q[m] + RP2];
+            }
+            // phase 2: local solves; phase 3: stores (points of one plane are never neighbours)
+#pragma unroll
+            for (int m = 0; m < PPT; ++m) {
+                if (!on[m]) continue;
+                const int pp = p[m];
+                sA[pp] = 0;                                                // Alg. 2 line 4
+                const T hf = fabs(hs[m]);
+                const T mx = fmin(xm[m], xp[m]), my = fmin(ym[m], yp[m]), mz = fmin(zm[m], zp[m]);
+                if (!(hf < INF) || !(fmin(mx, fmin(my, mz)) < v[m])) continue;   // fixed / no gain
+                ++nupd;
+                const T u = local_solve_fast<T>(mx, my, mz, hf);            // line 5
+                if (!(u < v[m])) continue;                                   // line 6
+                sV[q[m]] = u;                                                // line 7
+                if (hs[m] > T(0)) sH[pp] = -hs[m];                           // mark changed
+                ++nwr;
+                // lines 8-13: activate larger neighbours (predicated stores; the cross-border
+                // "currently downwind" test is done once per processing)
+                const int i = pp & (R - 1), j = (pp / R) & (R - 1), k = pp / (R * R);
+                if (xm[m] > u && i > 0) sA[pp - 1] = 1;
+                if (xp[m] > u && i < R - 1) sA[pp + 1] = 1;
+                if (ym[m] > u && j > 0) sA[pp - R] = 1;
+                if (yp[m] > u && j < R - 1) sA[pp + R] = 1;
+                if (zm[m] > u && k > 0) sA[pp - R * R] = 1;
+                if (zp[m] > u && k < R - 1) sA[pp + R * R] = 1;
+                myfwd |= ((fx ? xm[m] : xp[m]) > u) | ((fy ? ym[m] : yp[m]) > u) | ((fz ? zm[m] : zp[m]) > u);
+                bwd |= (((fx ? xp[m] : xm[m]) > u) && (fx ? i < R - 1 : i > 0) ? 1u : 0u) |
+                       (((fy ? yp[m] : ym[m]) > u) && (fy ? j < R - 1 : j > 0) ? 2u : 0u) |
+                       (((fz ? zp[m] : zm[m]) > u) && (fz ? k < R - 1 : k > 0) ? 4u : 0u);
             }
             fwd = __syncthreads_or(myfwd);
             ++nsteps;
         }
+#undef EIK_PREFETCH
         tstep += clock64() - tm1;
         nact = LCAP + 1;   // unknown until the next scan
         for (int o = 16; o > 0; o >>= 1) bwd |= __shfl_xor_sync(0xffffffffu, bwd, o);

@@ -479,7 +479,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     CK(cudaMemcpyAsync(ctx->ctl, ctx->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s));
     const int G = ctx->sm_count * 8;
     k_init_cells<<<G, 256, 0, s>>>(ctx->key, ctx->state, J);
-    Geom g{n1, cps, r};
+    Geom g{n1, cps, r, r == 4 ? 2 : r == 8 ? 3 : 4};
     k_ingest<T><<<G * 2, 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt, (T*)ctx->Ht,
                                       ctx->key, ctx->state, ctx->ctl, P);
     if (ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
@@ -521,7 +521,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
         return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
     if (ctx->ctl_host->abort)
         return fail(ctx, EIK_EINTERNAL, "processing limit exceeded (async scheduler)");
-    k_egress<T><<<G * 2, 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
+    k_egress<T><<<(int)(n1 * n1 < (int64_t)G * 16 ? n1 * n1 : (int64_t)G * 16), 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[3], s));
     CK(cudaEventSynchronize(ctx->ev[3]));

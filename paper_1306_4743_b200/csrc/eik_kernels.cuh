@@ -160,6 +160,7 @@ struct Geom {
     int64_t n1;        // n + 1 points per side
     int32_t cps;       // cells per side
     int32_t r;
+    int32_t lr;        // log2(r)
 };
 
 __device__ __forceinline__ void warp_agg_append(uint32_t* counter, uint32_t* list, uint32_t val,
@@ -186,17 +187,20 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
                          uint32_t* __restrict__ key, uint32_t* __restrict__ state, Ctl* ctl,
                          int64_t P)
 {
-    const int r = g.r, r3 = r * r * r;
+    const int r = g.r, lr = g.lr;
     const int64_t n1 = g.n1;
-    const int cps = g.cps;
+    const uint32_t cps = (uint32_t)g.cps;
     uint32_t exits = 0;
+    // shift/mask index math (r a power of two); one 32-bit division pair per point for the
+    // cell coordinates (J < 2^31)
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
          p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = p / r3;
-        const int e = (int)(p - c * r3);
-        const int a = e % r, b = (e / r) % r, d = e / (r * r);
-        const int cx = (int)(c % cps), cy = (int)((c / cps) % cps), cz = (int)(c / ((int64_t)cps * cps));
-        const int64_t i = (int64_t)cx * r + a, j = (int64_t)cy * r + b, k = (int64_t)cz * r + d;
+        const uint32_t c = (uint32_t)(p >> (3 * lr));
+        const int e = (int)(p & ((1 << (3 * lr)) - 1));
+        const int a = e & (r - 1), b = (e >> lr) & (r - 1), d = e >> (2 * lr);
+        const uint32_t cxy = c % (cps * cps);
+        const int cx = (int)(cxy % cps), cy = (int)(cxy / cps), cz = (int)(c / (cps * cps));
+        const int64_t i = (int64_t)(cx << lr) + a, j = (int64_t)(cy << lr) + b, k = (int64_t)(cz << lr) + d;
         T v = dinf<T>(), hf = dinf<T>();
         if (i < n1 && j < n1 && k < n1) {
             const int64_t lex = i + n1 * (j + n1 * k);
@@ -213,12 +217,13 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
                 // neighbour of an exit across a cell face are seeded too (R18)
                 atomicMin(&key[c], kb);
                 atomicOr(&state[c], FLAG_INIT);
-                const int64_t cc[6] = {a == 0 && i > 0 ? c - 1 : -1,
-                                       a == r - 1 && i + 1 < n1 ? c + 1 : -1,
-                                       b == 0 && j > 0 ? c - cps : -1,
-                                       b == r - 1 && j + 1 < n1 ? c + cps : -1,
-                                       d == 0 && k > 0 ? c - (int64_t)cps * cps : -1,
-                                       d == r - 1 && k + 1 < n1 ? c + (int64_t)cps * cps : -1};
+                const int64_t c64 = (int64_t)c, cp = (int64_t)cps;
+                const int64_t cc[6] = {a == 0 && i > 0 ? c64 - 1 : -1,
+                                       a == r - 1 && i + 1 < n1 ? c64 + 1 : -1,
+                                       b == 0 && j > 0 ? c64 - cp : -1,
+                                       b == r - 1 && j + 1 < n1 ? c64 + cp : -1,
+                                       d == 0 && k > 0 ? c64 - cp * cp : -1,
+                                       d == r - 1 && k + 1 < n1 ? c64 + cp * cp : -1};
 #pragma unroll
                 for (int f2 = 0; f2 < 6; ++f2)
                     if (cc[f2] >= 0) {
@@ -1156,15 +1161,20 @@ __global__ void k_seed_queue(uint32_t* state, uint32_t* ring, Ctl* ctl, int64_t 
 template <typename T>
 __global__ void k_egress(Geom g, const T* __restrict__ Vt, T* __restrict__ U, int64_t M)
 {
-    const int r = g.r, r3 = r * r * r;
+    // one (j, k) row of the output per block iteration: coalesced writes along i, tile reads
+    // in runs of r
+    const int r = g.r, lr = g.lr;
     const int64_t n1 = g.n1;
-    const int cps = g.cps;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < M;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = idx % n1, j = (idx / n1) % n1, k = idx / (n1 * n1);
-        const int64_t c = (i / r) + cps * ((j / r) + (int64_t)cps * (k / r));
-        const int e = (int)(i % r) + r * (int)(j % r) + r * r * (int)(k % r);
-        U[idx] = Vt[c * r3 + e];
+    const int64_t cps = g.cps;
+    const int64_t rows = n1 * n1;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int64_t k = row / n1, j = row - k * n1;
+        const int64_t cjk = cps * ((j >> lr) + cps * (k >> lr));
+        const int ejk = r * ((int)(j & (r - 1)) + r * (int)(k & (r - 1)));
+        for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) {
+            const int64_t c = (i >> lr) + cjk;
+            U[row * n1 + i] = Vt[(c << (3 * lr)) + ejk + (int)(i & (r - 1))];
+        }
     }
 }
 

@@ -63,8 +63,8 @@ typedef enum {
                                 while a neighbour runs [1], 2 also while a neighbour is queued
                                 with a smaller key, 3 ... with a key smaller by > bin width     */
     EIK_OPT_MAX_SWEEPS = 6   /* sweeps per cell processing before the cell saves its active
-                                points and re-queues itself (bounds round length); 0 = until
-                                convergence [0]                                                  */
+                                points and re-queues itself (bounds the round length, which is
+                                the slowest cell's); 0 = until convergence [4]                   */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */

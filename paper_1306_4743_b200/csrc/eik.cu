@@ -31,7 +31,7 @@ struct eik_ctx {
     int collect_stats = 1;
     int time_cell_events = 0;
     int async_defer = 1;
-    int max_sweeps = 0;
+    int max_sweeps = 4;
     cudaEvent_t cev[2] = {nullptr, nullptr};
     double ms_cell_events = 0;
     // scratch

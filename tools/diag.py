@@ -11,7 +11,7 @@ import paper_1306_4743_b200 as eik  # noqa: E402
 
 cfgs = sys.argv[1:] or ["C3"]
 for name in cfgs:
-    bw, mode, defer, msw = None, 2, 1, 0
+    bw, mode, defer, msw = None, 2, 1, 4
     if ":" in name:
         parts = name.split(":")
         name = parts[0]

@@ -62,9 +62,11 @@ typedef enum {
     EIK_OPT_ASYNC_DEFER = 5, /* async mode readiness test on a popped cell: 0 none, 1 defer
                                 while a neighbour runs [1], 2 also while a neighbour is queued
                                 with a smaller key, 3 ... with a key smaller by > bin width     */
-    EIK_OPT_MAX_SWEEPS = 6   /* sweeps per cell processing before the cell saves its active
+    EIK_OPT_MAX_SWEEPS = 6,  /* sweeps per cell processing before the cell saves its active
                                 points and re-queues itself (bounds the round length, which is
                                 the slowest cell's); 0 = until convergence [4]                   */
+    EIK_OPT_TIMEOUT_S = 7    /* device-side watchdog: the scheduler loop stops and the solve
+                                returns EIK_EINTERNAL after this many seconds [120]              */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */
@@ -136,7 +138,8 @@ int eik_get_stats(const eik_ctx* ctx, eik_stats* out);
  * out[3] processings, out[4 + s] number of processings that ran s sweeps (s = 31: >= 31),
  * out[36..39] cycles in staging / plane-mask / plane steps / write-back, out[40] active-list
  * iterations, out[41] async-mode deferrals, out[42 + 2r], out[43 + 2r] = cells and span (ns) of
- * round r (round modes, r < 1024).  Copies min(n, 42 + 2048) values.  EIK_EINVAL if ctx/out is NULL or n < 0. */
+ * round r (round modes, r < 1024), out[2090], out[2091] cycles in tile loads / halo loads.
+ * Copies min(n, 2092) values.  EIK_EINVAL if ctx/out is NULL or n < 0. */
 int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n);
 
 /* Message of the last failing call on ctx (owned by ctx; valid until its next call).

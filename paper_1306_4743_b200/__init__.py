@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libeik.so")
 EIK_OK, EIK_EINVAL, EIK_ENOMEM, EIK_ECUDA, EIK_ENOTSUP, EIK_EINTERNAL = range(6)
 EIK_F32, EIK_F64 = 0, 1
 (EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS,
- EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS) = range(7)
+ EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS, EIK_OPT_TIMEOUT_S) = range(8)
 STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
                 4: "EIK_ENOTSUP", 5: "EIK_EINTERNAL"}
 
@@ -178,12 +178,13 @@ class Solver:
 
     def debug(self) -> dict:
         import numpy as np
-        a = np.zeros(42, dtype=np.uint64)
-        lib.eik_get_debug(self._ctx, a.ctypes.data, 42)
+        a = np.zeros(2092, dtype=np.uint64)
+        lib.eik_get_debug(self._ctx, a.ctypes.data, 2092)
         return {"cycles_sum": int(a[0]), "cycles_max": int(a[1]), "plane_steps": int(a[2]),
                 "processings": int(a[3]), "sweep_hist": [int(x) for x in a[4:36]],
                 "cyc_stage": int(a[36]), "cyc_mask": int(a[37]), "cyc_steps": int(a[38]),
-                "cyc_writeback": int(a[39]), "list_iters": int(a[40]), "defers": int(a[41])}
+                "cyc_writeback": int(a[39]), "list_iters": int(a[40]), "defers": int(a[41]),
+                "cyc_tile": int(a[2090]), "cyc_halo": int(a[2091])}
 
     def stats(self) -> dict:
         s = EikStats()

@@ -9,6 +9,8 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <time.h>
+#include <unistd.h>
 
 #include <string>
 #include <vector>
@@ -32,6 +34,7 @@ struct eik_ctx {
     int time_cell_events = 0;
     int async_defer = 1;
     int max_sweeps = 4;
+    double timeout_s = 120.0;
     cudaEvent_t cev[2] = {nullptr, nullptr};
     double ms_cell_events = 0;
     // scratch
@@ -238,6 +241,10 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         if (value < 0 || value > 5) return fail(ctx, EIK_EINVAL, "defer mode must be 0..5");
         ctx->async_defer = (int)value;
         return EIK_OK;
+    case EIK_OPT_TIMEOUT_S:
+        if (!(value > 0)) return fail(ctx, EIK_EINVAL, "timeout must be > 0 s");
+        ctx->timeout_s = value;
+        return EIK_OK;
     case EIK_OPT_MAX_SWEEPS:
         if (!(value >= 0) || value > 1e6) return fail(ctx, EIK_EINVAL, "max sweeps must be >= 0");
         ctx->max_sweeps = (int)value;
@@ -265,6 +272,8 @@ extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
     for (int i = 0; i < m; ++i) out[i] = ctx->ctl_host->dbg[i];
     if (n > 41) out[41] = ctx->ctl_host->defers;
     for (int i = 42; i < n && i < 42 + 2048; ++i) out[i] = ctx->ctl_host->rtrace[i - 42];
+    if (n > 42 + 2048) out[42 + 2048] = ctx->ctl_host->dbg[41];
+    if (n > 43 + 2048) out[43 + 2048] = ctx->ctl_host->dbg[42];
     return EIK_OK;
 }
 
@@ -473,12 +482,13 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     init.kmin[0] = init.kmin[1] = KEY_INF;
     init.max_rounds = ctx->max_rounds;
     init.t_start = ~0ull;
+    init.budget_ns = (unsigned long long)(ctx->timeout_s * 1e9);
     ctx->ms_cell_events = 0;
     *ctx->ctl_host = init;
     CK(cudaEventRecord(ctx->ev[0], s));
     CK(cudaMemcpyAsync(ctx->ctl, ctx->ctl_host, sizeof(Ctl), cudaMemcpyHostToDevice, s));
     const int G = ctx->sm_count * 8;
-    k_init_cells<<<G, 256, 0, s>>>(ctx->key, ctx->state, J);
+    k_init_cells<<<G, 256, 0, s>>>(ctx->key, ctx->state, J, ctx->ctl);
     Geom g{n1, cps, r, r == 4 ? 2 : r == 8 ? 3 : 4};
     k_ingest<T><<<G * 2, 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt, (T*)ctx->Ht,
                                       ctx->key, ctx->state, ctx->ctl, P);
@@ -515,10 +525,43 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     st = run_loop<T>(ctx, r, J, ca);
     if (st) return st;
     CK(cudaEventRecord(ctx->ev[2], s));
+    // host-side guard against a device loop that never returns (the device watchdog covers
+    // the scheduler; this covers everything else): poll the loop-end event with a deadline
+    {
+        const double limit_s = ctx->timeout_s + 30.0;
+        struct timespec t0, t1;
+        clock_gettime(CLOCK_MONOTONIC, &t0);
+        for (;;) {
+            const cudaError_t q = cudaEventQuery(ctx->ev[2]);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) CK(q);
+            clock_gettime(CLOCK_MONOTONIC, &t1);
+            if ((t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec) > limit_s) {
+                // read the control block through a side stream while the loop still runs
+                cudaStream_t side;
+                Ctl snap;
+                if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess) {
+                    cudaMemcpyAsync(&snap, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, side);
+                    cudaStreamSynchronize(side);
+                    cudaStreamDestroy(side);
+                }
+                return fail(ctx, EIK_EINTERNAL, "device loop did not finish in %.0f s (pending %u head %u "
+                            "tail %u rounds %u processings %llu); the context is unusable",
+                            limit_s, snap.pending, snap.q_head, snap.q_tail, snap.rounds,
+                            (unsigned long long)snap.processings);
+            }
+            usleep(200);
+        }
+    }
     CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (ctx->ctl_host->err & 4u)
         return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
+    if (ctx->ctl_host->err & 8u)
+        return fail(ctx, EIK_EINTERNAL, "watchdog: solve exceeded %.1f s (pending %u head %u tail %u "
+                    "rounds %u processings %llu)", ctx->timeout_s, ctx->ctl_host->pending,
+                    ctx->ctl_host->q_head, ctx->ctl_host->q_tail, ctx->ctl_host->rounds,
+                    (unsigned long long)ctx->ctl_host->processings);
     if (ctx->ctl_host->abort)
         return fail(ctx, EIK_EINTERNAL, "processing limit exceeded (async scheduler)");
     k_egress<T><<<(int)(n1 * n1 < (int64_t)G * 16 ? n1 * n1 : (int64_t)G * 16), 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);

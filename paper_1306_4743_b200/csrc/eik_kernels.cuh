@@ -135,12 +135,13 @@ struct Ctl {
     unsigned long long t_start, t_end;     // this round's cell-kernel span (%globaltimer ns)
     unsigned long long cell_ns, cell_launches;
     uint32_t q_head, q_tail, pending, abort;   // async mode ring + work counter
+    unsigned long long t_solve0, budget_ns;     // watchdog: abort after budget_ns
     uint32_t rtrace[2048];                      // round mode: per-round (cells, span ns)
     uint32_t claim;                             // round mode: next cell of this round
     unsigned long long defers;
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
     // steps executed, [3] processings, [4..35] histogram of sweeps per processing (31 = >=31)
-    unsigned long long dbg[41];   // [36] stage, [37] plane-mask, [38] steps, [39] write-back cycles, [40] list iterations
+    unsigned long long dbg[43];   // [36] stage, [37] plane-mask, [38] steps, [39] write-back cycles, [40] list iterations
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -242,8 +243,9 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
     if ((threadIdx.x & 31) == 0 && exits) atomicAdd(&ctl->n_exits, exits);
 }
 
-__global__ void k_init_cells(uint32_t* key, uint32_t* state, int64_t J)
+__global__ void k_init_cells(uint32_t* key, uint32_t* state, int64_t J, Ctl* ctl)
 {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->t_solve0 = gtimer();   // watchdog origin
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < J;
          c += (int64_t)gridDim.x * blockDim.x) {
         key[c] = KEY_INF;
@@ -332,8 +334,9 @@ __device__ __forceinline__ bool round_end_body(Ctl* ctl)
     ctl->wl_count[cur] = 0;
     ctl->kmin[cur] = KEY_INF;
     ctl->cur = nx;
-    const bool more = ctl->wl_count[nx] != 0;
+    bool more = ctl->wl_count[nx] != 0;
     if (more && ctl->rounds >= ctl->max_rounds) ctl->err |= 4u;
+    if (more && gtimer() - ctl->t_solve0 > ctl->budget_ns) { ctl->err |= 8u; more = false; }   // watchdog
     ctl->done = (more && ctl->rounds < ctl->max_rounds) ? 0u : 1u;
     return ctl->done != 0u;
 }
@@ -406,6 +409,10 @@ __device__ __forceinline__ uint32_t pref_dirs(uint32_t faces)
     return m;
 }
 
+template <typename T> struct Vec16;
+template <> struct Vec16<float> { using type = float4; };
+template <> struct Vec16<double> { using type = double2; };
+
 // Shared-memory state of one cell processing (static part; the big arrays are dynamic).
 template <int R> struct CellShared {
     int32_t off[CellCfg<R>::NPL + 1];  // plane offsets into the plane table
@@ -419,6 +426,7 @@ template <int R> struct CellShared {
     int32_t nact, nact2[2];            // active-point counts
     int32_t lcnt[2], lover;            // active-list lengths / overflow
     uint32_t bwd[2];                   // axes with activations behind the wavefront
+    unsigned long long plane0;         // active planes of the first sweep (direction dir0)
 };
 
 // dynamic shared memory carve-up
@@ -492,35 +500,49 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     if (tid < 6) S.face_min[tid] = KEY_INF;
     if (tid == 0) {
         S.face_flag = 0; S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
+        S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
     }
-    long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0, nlist = 0;
+    long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0, nlist = 0, tsa = 0, tsb = 0;
     constexpr int NWB = R3 / 32;   // saved-bitmask words
 
-    // ---- stage V and hf (coalesced), then the halo N(c): all loads of a batch are issued
-    // before any store so that many are in flight per thread (memory-level parallelism) ----
+    // ---- stage V and hf with 16-byte vector loads (all of a batch in flight before any
+    // store: memory-level parallelism), then the halo N(c) ----
     const bool init = flags & FLAG_INIT;
     {
-        constexpr int PER = (R3 + NT - 1) / NT;          // tile elements per thread
-        constexpr int B = sizeof(T) == 4 ? (PER + 1) / 2 : (PER + 3) / 4;   // batch
+        using V4 = typename Vec16<T>::type;
+        constexpr int EL = 16 / sizeof(T);                // elements per vector
+        constexpr int NV = R3 / EL;                       // vectors per tile
+        constexpr int PV = (NV + NT - 1) / NT;            // vectors per thread
+        constexpr int B = sizeof(T) == 4 ? 3 : 2;           // batch (register budget)
+        const V4* Vt4 = reinterpret_cast<const V4*>(Vt + base);
+        const V4* Ht4 = reinterpret_cast<const V4*>(Ht + base);
+        V4* sH4 = reinterpret_cast<V4*>(sH);
 #pragma unroll
-        for (int m0 = 0; m0 < PER; m0 += B) {
-            T va[B], ha[B];
+        for (int m0 = 0; m0 < PV; m0 += B) {
+            V4 va[B], ha[B];
 #pragma unroll
             for (int m = 0; m < B; ++m) {
-                const int e = tid + (m0 + m) * NT;
-                if (m0 + m < PER && e < R3) { va[m] = __ldcg(&Vt[base + e]); ha[m] = __ldcg(&Ht[base + e]); }
+                const int vi = tid + (m0 + m) * NT;
+                if (m0 + m < PV && vi < NV) { va[m] = __ldcg(&Vt4[vi]); ha[m] = __ldcg(&Ht4[vi]); }
             }
 #pragma unroll
             for (int m = 0; m < B; ++m) {
-                const int e = tid + (m0 + m) * NT;
-                if (m0 + m < PER && e < R3) {
-                    const int a = e % R, b = (e / R) % R, d = e / (R * R);
-                    sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = va[m];
-                    sH[e] = ha[m];
+                const int vi = tid + (m0 + m) * NT;
+                if (m0 + m < PV && vi < NV) {
+                    sH4[vi] = ha[m];
+                    const T* pv = reinterpret_cast<const T*>(&va[m]);
+#pragma unroll
+                    for (int l = 0; l < EL; ++l) {
+                        const int e = vi * EL + l;
+                        const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+                        sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = pv[l];
+                    }
                 }
             }
         }
+        __syncthreads();
+        tsa = clock64();
         constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
         T hv[PH];
         int hq[PH];
@@ -553,35 +575,74 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     __syncthreads();
     // ---- initial activity: all points (INIT), or the points of the inflow faces whose
     // outside neighbour is smaller (only smaller neighbours enter Eq. (2)), plus the
-    // points saved at a sweep cap ----
+    // points saved at a sweep cap.  The first sweep's direction is fixed by the inflow faces,
+    // so its set of active planes is collected here (no separate scan) ----
+    __syncthreads();
+    tsb = clock64();
+    const int dir0 = (init || !(flags & 63u)) ? 0 :
+        (((flags & 2u) && !(flags & 1u) ? 1 : 0) | ((flags & 8u) && !(flags & 4u) ? 2 : 0) |
+         ((flags & 32u) && !(flags & 16u) ? 4 : 0));
     {
         int cnt = 0;
-        for (int e = tid; e < R3; e += NT) {
-            const int a = e % R, b = (e / R) % R, d = e / (R * R);
-            bool on = init;
-            if (!on && (flags & 63u)) {
+        unsigned long long pm0 = 0;
+        auto plane0 = [&](int a, int b, int d) {
+            return ((dir0 & 1) ? R - 1 - a : a) + ((dir0 & 2) ? R - 1 - b : b) + ((dir0 & 4) ? R - 1 - d : d);
+        };
+        uint32_t* sA32 = reinterpret_cast<uint32_t*>(sA);
+        if (init) {
+            for (int w = tid; w < R3 / 4; w += NT) sA32[w] = 0x01010101u;
+            cnt = tid == 0 ? R3 : 0;
+            pm0 = tid == 0 ? ((1ull << NPL) - 1ull) : 0ull;
+        } else {
+            for (int w = tid; w < R3 / 4; w += NT) sA32[w] = 0u;
+            __syncthreads();
+            // face points whose outside neighbour is smaller
+            for (int e = tid; e < 6 * R * R; e += NT) {
+                const int f = e / (R * R);
+                if (!(flags & (1u << f))) continue;
+                const int uv = e - f * R * R, u = uv & (R - 1), v = uv / R;
+                int a, b, d, off;
+                switch (f) {
+                case 0: a = 0; b = u; d = v; off = -1; break;
+                case 1: a = R - 1; b = u; d = v; off = 1; break;
+                case 2: a = u; b = 0; d = v; off = -RP; break;
+                case 3: a = u; b = R - 1; d = v; off = RP; break;
+                case 4: a = u; b = v; d = 0; off = -RP2; break;
+                default: a = u; b = v; d = R - 1; off = RP2; break;
+                }
                 const int q = (a + 1) + RP * (b + 1) + RP2 * (d + 1);
-                const T v = sV[q];
-                on = ((flags & 1u) && a == 0 && sV[q - 1] < v) ||
-                     ((flags & 2u) && a == R - 1 && sV[q + 1] < v) ||
-                     ((flags & 4u) && b == 0 && sV[q - RP] < v) ||
-                     ((flags & 8u) && b == R - 1 && sV[q + RP] < v) ||
-                     ((flags & 16u) && d == 0 && sV[q - RP2] < v) ||
-                     ((flags & 32u) && d == R - 1 && sV[q + RP2] < v);
+                if (sV[q + off] < sV[q]) {
+                    sA[a + R * b + R * R * d] = 1;
+                    ++cnt;
+                    pm0 |= 1ull << plane0(a, b, d);
+                }
             }
-            if ((flags & FLAG_CONT) && !on)
-                on = (__ldcg(&A.pend[(int64_t)c * NWB + (e >> 5)]) >> (e & 31)) & 1u;
-            sA[e] = on ? 1 : 0;
-            cnt += on;
+            // points saved at a sweep cap
+            if (flags & FLAG_CONT) {
+                for (int w = tid; w < NWB; w += NT) {
+                    uint32_t x = __ldcg(&A.pend[(int64_t)c * NWB + w]);
+                    while (x) {
+                        const int e = 32 * w + __ffs(x) - 1;
+                        x &= x - 1;
+                        sA[e] = 1;
+                        ++cnt;
+                        pm0 |= 1ull << plane0(e & (R - 1), (e / R) & (R - 1), e / (R * R));
+                    }
+                }
+            }
         }
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if ((tid & 31) == 0 && cnt) atomicAdd(&S.nact, cnt);
+        for (int o = 16; o > 0; o >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            pm0 |= __shfl_xor_sync(0xffffffffu, pm0, o);
+        }
+        if ((tid & 31) == 0 && cnt) { atomicAdd(&S.nact, cnt); atomicOr(&S.plane0, pm0); }
     }
     __syncthreads();
     const long long tc1 = clock64();
 
     int gi = 0, prev_dir = -1;
     int lf0 = -1, lf1 = -1, lf2 = -1;   // sweep at which each axis was last reversed
+    bool ran_list = false;
     uint32_t nsweeps = 0;
     uint32_t nupd = 0, nwr = 0;
     int nact = S.nact;     // active points (exact at loop entry)
@@ -589,6 +650,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         if (nact == 0) break;
         // ================= active-list relaxation (few active points) =================
         if (nact <= LCAP) {
+            ran_list = true;
             const long long tl0 = clock64();
             // build the list from the flags
             if (tid == 0) { S.lcnt[0] = 0; S.lcnt[1] = 0; S.lover = 0; }
@@ -680,11 +742,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             const uint32_t bw = sw > 0 ? S.bwd[(sw - 1) & 1] : 0u;
             if (tid == 0) S.bwd[sw & 1] = 0;
             if (prev_dir < 0) {
-                if (init || !(flags & 63u)) { dir = 0; gi = 1; }
-                else {
-                    dir = ((flags & 2u) && !(flags & 1u) ? 1 : 0) | ((flags & 8u) && !(flags & 4u) ? 2 : 0) |
-                          ((flags & 32u) && !(flags & 16u) ? 4 : 0);
-                }
+                dir = dir0;
+                if (init || !(flags & 63u)) gi = 1;
             } else if (bw) {
                 // flip one of those axes per sweep, the least recently flipped one (a source
                 // inside the cell needs all 8 octants: this then walks a Gray cycle)
@@ -703,8 +762,10 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         const bool fx = dir & 1, fy = dir & 2, fz = dir & 4;
         const long long tm0 = clock64();
-        // the set of planes (in this direction) holding active points, and their count
-        {
+        // the set of planes (in this direction) holding active points, and their count (the
+        // first sweep's was collected with the initial activity)
+        const bool first = sw == 0 && !ran_list;
+        if (!first) {
             unsigned long long pm = 0;
             int cnt = 0;
             const uint32_t* sA32 = reinterpret_cast<const uint32_t*>(sA);
@@ -713,7 +774,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 while (x) {
                     const int e = 4 * wd + ((__ffs(x) - 1) >> 3);
                     x &= ~(0xffu << (8 * (e & 3)));
-                    const int a = e % R, b = (e / R) % R, d = e / (R * R);
+                    const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
                     pm |= 1ull << ((fx ? R - 1 - a : a) + (fy ? R - 1 - b : b) + (fz ? R - 1 - d : d));
                     ++cnt;
                 }
@@ -724,10 +785,10 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
             }
             if ((tid & 31) == 0 && pm) { atomicOr(&S.plane[sw & 1], pm); atomicAdd(&S.nact2[sw & 1], cnt); }
+            __syncthreads();
         }
-        __syncthreads();
-        const unsigned long long pm = S.plane[sw & 1];
-        nact = S.nact2[sw & 1];
+        const unsigned long long pm = first ? S.plane0 : S.plane[sw & 1];
+        nact = first ? S.nact : S.nact2[sw & 1];
         if (tid == 0) { S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0; }
         const long long tm1 = clock64();
         tmask += tm1 - tm0;
@@ -879,13 +940,33 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     }
     __syncthreads();
 
-    // ---- write back changed values only (coalesced) ----
+    // ---- write back (16-byte vectors; a vector holding any changed point is stored whole,
+    // unchanged values are rewritten identically) ----
     unsigned long long nw = 0;
-    for (int e = tid; e < R3; e += NT) {
-        if (sH[e] < T(0)) {
-            const int a = e % R, b = (e / R) % R, d = e / (R * R);
-            __stcg(&Vt[base + e], sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)]);
-            ++nw;
+    {
+        using V4 = typename Vec16<T>::type;
+        constexpr int EL = 16 / sizeof(T);
+        constexpr int NV = R3 / EL;
+        V4* Vt4 = reinterpret_cast<V4*>(Vt + base);
+        const V4* sH4 = reinterpret_cast<const V4*>(sH);
+        for (int vi = tid; vi < NV; vi += NT) {
+            const V4 hv = sH4[vi];
+            const T* ph = reinterpret_cast<const T*>(&hv);
+            int nchg = 0;
+#pragma unroll
+            for (int l = 0; l < EL; ++l) nchg += ph[l] < T(0);
+            if (nchg) {
+                V4 out;
+                T* po = reinterpret_cast<T*>(&out);
+#pragma unroll
+                for (int l = 0; l < EL; ++l) {
+                    const int e = vi * EL + l;
+                    const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+                    po[l] = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
+                }
+                __stcg(&Vt4[vi], out);
+                nw += nchg;
+            }
         }
     }
     if (A.stats) {
@@ -904,6 +985,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     n_sweeps_out = nsweeps;
     if (tid == 0 && A.stats) {
         atomicAdd(&A.ctl->dbg[36], (unsigned long long)(tc1 - tc0));
+        atomicAdd(&A.ctl->dbg[41], (unsigned long long)(tsa - tc0));
+        atomicAdd(&A.ctl->dbg[42], (unsigned long long)(tsb - tsa));
         atomicAdd(&A.ctl->dbg[37], (unsigned long long)tmask);
         atomicAdd(&A.ctl->dbg[38], (unsigned long long)tstep);
         atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - tc2));
@@ -1050,8 +1133,13 @@ k_async(CellArgs A)
             unsigned ns = 32;
             for (;;) {
                 if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) break;
+                if (gtimer() - __ldcg(&ctl->t_solve0) > __ldcg(&ctl->budget_ns)) {   // watchdog
+                    atomicOr(&ctl->err, 8u);
+                    atomicExch(&ctl->abort, 1u);
+                    break;
+                }
                 const uint32_t h = __ldcg(&ctl->q_head), t = __ldcg(&ctl->q_tail);
-                if (h != t) {
+                if ((int32_t)(t - h) > 0) {   // never claim past the tail (the two loads are unordered)
                     if (atomicCAS(&ctl->q_head, h, h + 1u) == h) {
                         uint32_t v;
                         while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) __nanosleep(20);

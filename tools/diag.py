@@ -38,6 +38,6 @@ for name in cfgs:
            "steps_per_proc": dbg["plane_steps"] / p, "sweeps_per_proc": st["cell_sweeps"] / p,
            "upd_per_proc": st["point_updates"] / p, "hist": dbg["sweep_hist"][:16],
            "stage": dbg["cyc_stage"] / p, "mask": dbg["cyc_mask"] / p, "stepcyc": dbg["cyc_steps"] / p,
-           "wb": dbg["cyc_writeback"] / p, "list_it": dbg["list_iters"] / p, "cyc_per_step": dbg["cyc_steps"] / max(dbg["plane_steps"], 1)}
+           "wb": dbg["cyc_writeback"] / p, "tile": dbg["cyc_tile"] / p, "halo": dbg["cyc_halo"] / p, "list_it": dbg["list_iters"] / p, "cyc_per_step": dbg["cyc_steps"] / max(dbg["plane_steps"], 1)}
     print(json.dumps(out))
     s.close()

@@ -7,7 +7,7 @@ cfg, prec, r = bench.WORKLOADS[name]
 n, F, m, q = bench.make_inputs(cfg, prec, torch.device("cuda", 0))
 s = eik.Solver(loop_mode=2)
 s.solve(F, m, q, cell_size=r, n=n); s.solve(F, m, q, cell_size=r, n=n)
-a = np.zeros(42 + 2048, dtype=np.uint64)
+a = np.zeros(2092, dtype=np.uint64)
 eik.lib.eik_get_debug(s._ctx, a.ctypes.data, len(a))
 st = s.stats()
 tr = a[42:].reshape(-1, 2)[:st["rounds"]]

@@ -76,7 +76,7 @@ __device__ __forceinline__ double sqrt_fast(double x) { return __dsqrt_rn(x); }
 __device__ __forceinline__ float sqrt_approx(float x)
 {
     float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));   // arguments are O(hf^2) >> FLT_MIN
     return r;
 }
 __device__ __forceinline__ double sqrt_approx(double x) { return __dsqrt_rn(x); }
@@ -366,7 +366,7 @@ template <typename T, int R>
 constexpr size_t cell_smem_bytes()
 {
     // V box + hf + plane table (uint16) + active bytes + 2 active lists (uint16)
-    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + 3 * CellCfg<R>::R3 + 4 * CellCfg<R>::LCAP;
+    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + 3 * CellCfg<R>::R3 + 16 + 4 * CellCfg<R>::LCAP;
 }
 
 struct CellArgs {
@@ -442,7 +442,7 @@ template <typename T, int R> struct CellSmem {
         H = V + CellCfg<R>::BOX;
         tab = reinterpret_cast<uint16_t*>(H + CellCfg<R>::R3);
         act = reinterpret_cast<uint8_t*>(tab + CellCfg<R>::R3);
-        list = reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3);
+        list = reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3 + 16);   // act[R3] = scratch
     }
 };
 
@@ -503,7 +503,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
     }
-    long long tc0 = clock64(), tmask = 0, tstep = 0, nsteps = 0, nlist = 0, tsa = 0, tsb = 0;
+    long long tc0 = clock64(), tmask = 0, tstep = 0, nlist = 0, tsa = 0, tsb = 0;
+    uint32_t nsteps = 0;
     constexpr int NWB = R3 / 32;   // saved-bitmask words
 
     // ---- stage V and hf with 16-byte vector loads (all of a batch in flight before any
@@ -820,20 +821,24 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         bool fwd = false;
         uint32_t bwd = 0;
         int s = __ffsll((long long)pm) - 1;
-        // reflection of the canonical plane table for this direction: the index of a point is
-        // i + R j + R^2 k with R a power of two, so reflecting an axis is an XOR of its field
-        const int dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
-        // prefetch: the points this thread owns at plane sp (PPT slots) and their hf
-        int pn[PPT];
-        T hn[PPT];
+        // The plane table holds canonical (reflected) coordinates e = a + R b + R^2 c with
+        // a + b + c = s.  The point index is p = e XOR dm (R a power of two: reflecting an axis
+        // XORs its field); in canonical coordinates "forward" along an axis is +1 and the
+        // forward / backward neighbours exist iff the coordinate is < R-1 / > 0.  Box and flag
+        // offsets of the forward neighbours are per-sweep constants.
+        const unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
+        const int oxq = fx ? -1 : 1, oyq = fy ? -RP : RP, ozq = fz ? -RP2 : RP2;   // box
+        const int oxp = fx ? -1 : 1, oyp = fy ? -R : R, ozp = fz ? -R * R : R * R;  // flags
+        // prefetch: the canonical entry this thread owns at plane sp and its hf
+        int en = -1;
+        T hn = INF;
 #define EIK_PREFETCH(sp_)                                                                  \
         {                                                                                  \
             const int sp = (sp_);                                                          \
-            const int o0 = sp < NPL ? S.off[sp] : 0, o1 = sp < NPL ? S.off[sp + 1] : 0;    \
-            _Pragma("unroll") for (int m = 0; m < PPT; ++m) {                              \
-                const int e = o0 + tid + m * NT;                                           \
-                pn[m] = -1;                                                                \
-                if (e < o1) { pn[m] = (int)M.tab[e] ^ dm; hn[m] = sH[pn[m]]; }             \
+            en = -1;                                                                       \
+            if (sp < NPL) {                                                                \
+                const int e_ = S.off[sp] + tid;                                            \
+                if (e_ < S.off[sp + 1]) { en = M.tab[e_]; hn = sH[en ^ dm]; }              \
             }                                                                              \
         }
         EIK_PREFETCH(s)
@@ -844,56 +849,49 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 EIK_PREFETCH(s + 1)
                 continue;
             }
-            int p[PPT];
-            T hs[PPT];
-#pragma unroll
-            for (int m = 0; m < PPT; ++m) { p[m] = pn[m]; hs[m] = hn[m]; }
+            const int e = en;
+            const T hs = hn;
             EIK_PREFETCH(s + 1)   // independent of this step's results
             bool myfwd = false;
-            // phase 1: all loads (flags, then values of the active points)
-            bool on[PPT];
-            int q[PPT];
-            T v[PPT], xm[PPT], xp[PPT], ym[PPT], yp[PPT], zm[PPT], zp[PPT];
-#pragma unroll
-            for (int m = 0; m < PPT; ++m) on[m] = p[m] >= 0 && sA[p[m]];
-#pragma unroll
-            for (int m = 0; m < PPT; ++m) {
-                if (!on[m]) continue;
-                const int i = p[m] & (R - 1), j = (p[m] / R) & (R - 1), k = p[m] / (R * R);
-                q[m] = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
-                v[m] = sV[q[m]];
-                xm[m] = sV[q[m] - 1]; xp[m] = sV[q[m] + 1];
-                ym[m] = sV[q[m] - RP]; yp[m] = sV[q[m] + RP];
-                zm[m] = sV[q[m] - RP2]; zp[m] = sV[q[m] + RP2];
-            }
-            // phase 2: local solves; phase 3: stores (points of one plane are never neighbours)
-#pragma unroll
-            for (int m = 0; m < PPT; ++m) {
-                if (!on[m]) continue;
-                const int pp = p[m];
-                sA[pp] = 0;                                                // Alg. 2 line 4
-                const T hf = fabs(hs[m]);
-                const T mx = fmin(xm[m], xp[m]), my = fmin(ym[m], yp[m]), mz = fmin(zm[m], zp[m]);
-                if (!(hf < INF) || !(fmin(mx, fmin(my, mz)) < v[m])) continue;   // fixed / no gain
-                ++nupd;
-                const T u = local_solve_fast<T>(mx, my, mz, hf);            // line 5
-                if (!(u < v[m])) continue;                                   // line 6
-                sV[q[m]] = u;                                                // line 7
-                if (hs[m] > T(0)) sH[pp] = -hs[m];                           // mark changed
-                ++nwr;
-                // lines 8-13: activate larger neighbours (predicated stores; the cross-border
-                // "currently downwind" test is done once per processing)
-                const int i = pp & (R - 1), j = (pp / R) & (R - 1), k = pp / (R * R);
-                if (xm[m] > u && i > 0) sA[pp - 1] = 1;
-                if (xp[m] > u && i < R - 1) sA[pp + 1] = 1;
-                if (ym[m] > u && j > 0) sA[pp - R] = 1;
-                if (yp[m] > u && j < R - 1) sA[pp + R] = 1;
-                if (zm[m] > u && k > 0) sA[pp - R * R] = 1;
-                if (zp[m] > u && k < R - 1) sA[pp + R * R] = 1;
-                myfwd |= ((fx ? xm[m] : xp[m]) > u) | ((fy ? ym[m] : yp[m]) > u) | ((fz ? zm[m] : zp[m]) > u);
-                bwd |= (((fx ? xp[m] : xm[m]) > u) && (fx ? i < R - 1 : i > 0) ? 1u : 0u) |
-                       (((fy ? yp[m] : ym[m]) > u) && (fy ? j < R - 1 : j > 0) ? 2u : 0u) |
-                       (((fz ? zp[m] : zm[m]) > u) && (fz ? k < R - 1 : k > 0) ? 4u : 0u);
+            if (e >= 0) {
+                const unsigned ue = (unsigned)e;
+                const int p = (int)(ue ^ dm);
+                if (sA[p]) {
+                    sA[p] = 0;                                             // Alg. 2 line 4
+                    const unsigned up = (unsigned)p;
+                    const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
+                    const T v = sV[q];
+                    const T xf = sV[q + oxq], xb = sV[q - oxq];
+                    const T yf = sV[q + oyq], yb = sV[q - oyq];
+                    const T zf = sV[q + ozq], zb = sV[q - ozq];
+                    const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
+                    const T hf = fabs(hs);
+                    if (hf < INF && fmin(mx, fmin(my, mz)) < v) {          // fixed / no gain
+                        ++nupd;
+                        const T u = local_solve_fast<T>(mx, my, mz, hf);    // line 5
+                        if (u < v) {                                         // line 6
+                            sV[q] = u;                                       // line 7
+                            if (hs > T(0)) sH[p] = -hs;                      // mark changed
+                            ++nwr;
+                            // lines 8-13: activate larger in-cell neighbours (the cross-border
+                            // "currently downwind" test is done once per processing)
+                            const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
+                            // activations as unconditional byte stores to either the neighbour
+                            // or a scratch byte (short-lived compares, no predicate pressure)
+                            const int fxa = (xf > u) & (ca < R - 1), bxa = (xb > u) & (ca > 0);
+                            const int fya = (yf > u) & (cb < R - 1), bya = (yb > u) & (cb > 0);
+                            const int fza = (zf > u) & (cc < R - 1), bza = (zb > u) & (cc > 0);
+                            sA[fxa ? p + oxp : R3] = 1;
+                            sA[bxa ? p - oxp : R3] = 1;
+                            sA[fya ? p + oyp : R3] = 1;
+                            sA[bya ? p - oyp : R3] = 1;
+                            sA[fza ? p + ozp : R3] = 1;
+                            sA[bza ? p - ozp : R3] = 1;
+                            myfwd = (fxa | fya | fza) != 0;
+                            bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
+                        }
+                    }
+                }
             }
             fwd = __syncthreads_or(myfwd);
             ++nsteps;

@@ -9,6 +9,7 @@ ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "eik.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "eik_kernels.cuh"), os.path.join(ROOT, "include", "eik.h")]
 LIB = os.path.join(PKG, "libeik.so")
+LIB_CHECKS = os.path.join(PKG, "libeik_checks.so")   # -DEIK_CHECKS: device bounds checks
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include")]
@@ -21,12 +22,18 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def _nvcc(out, extra):
+    tmp = out + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, *FLAGS, *extra, "-o", tmp, *SRC])
+    os.replace(tmp, out)
+
+
+def build(force: bool = False, verbose: bool = False, checks: bool = True) -> str:
     if force or needs_build():
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp, *SRC]
-        subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
+        _nvcc(LIB, ["-Xptxas", "-v"] if verbose else [])
+    if checks and (force or not os.path.exists(LIB_CHECKS) or
+                   os.path.getmtime(LIB_CHECKS) < os.path.getmtime(LIB)):
+        _nvcc(LIB_CHECKS, ["-DEIK_CHECKS"])
     return LIB
 
 

@@ -517,6 +517,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.Vt = ctx->Vt;
     ca.Ht = ctx->Ht;
     ca.max_sweeps = ctx->max_sweeps;
+    ca.cap = (uint32_t)J;
     ca.pend = ctx->pend;
     ca.gen = ctx->gen;
     ca.n1 = n1;

@@ -23,6 +23,22 @@
 
 namespace eik {
 
+// Device-side bounds checks (build with -DEIK_CHECKS, library libeik_checks.so): a violated
+// invariant prints and traps.  compute-sanitizer is not available on the GPU pool, so the
+// checked build run over the GPU test suite stands in for memcheck on the indices we compute.
+#ifdef EIK_CHECKS
+#define EIK_CHECK(cond, what)                                                              \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("EIK_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__,    \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                           \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define EIK_CHECK(cond, what) do { } while (0)
+#endif
+
 // --------------------------------------------------------------------------------------
 // numeric helpers
 // --------------------------------------------------------------------------------------
@@ -391,6 +407,7 @@ struct CellArgs {
                                      // neighbours, 2 + smaller-key queued, 3 + key - delta)
     float defer_delta;
     int32_t max_sweeps;              // sweeps per processing before continuing later (0: none)
+    uint32_t cap;                    // number of cells J (bounds checks)
     uint32_t* pend;                  // J x R^3/32 saved active bits (FLAG_CONT)
 };
 
@@ -566,6 +583,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
                 }
                 hq[m] = (hx + 1) + RP * (hy + 1) + RP2 * (hz + 1);
+                EIK_CHECK(!ex || (nc >= 0 && nc < (int64_t)A.cap), "halo neighbour cell");
                 if (ex) hv[m] = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
             }
         }
@@ -679,6 +697,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 uint16_t* Ln = M.list + (cur ^ 1) * LCAP;
                 for (int t = tid; t < n; t += NT) {
                     const int p = Lc[t];
+                    EIK_CHECK(p >= 0 && p < R3, "list point index");
                     sA[p] = 0;                                               // Alg. 2 line 4
                     const T hs = sH[p];
                     const T hf = fabs(hs);
@@ -856,10 +875,12 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             if (e >= 0) {
                 const unsigned ue = (unsigned)e;
                 const int p = (int)(ue ^ dm);
+                EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
                 if (sA[p]) {
                     sA[p] = 0;                                             // Alg. 2 line 4
                     const unsigned up = (unsigned)p;
                     const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
+                    EIK_CHECK(q - RP2 >= 0 && q + RP2 < C::BOX, "box index");
                     const T v = sV[q];
                     const T xf = sV[q + oxq], xb = sV[q - oxq];
                     const T yf = sV[q + oyq], yb = sV[q - oyq];
@@ -1054,6 +1075,7 @@ k_cell(CellArgs A)
         worked = true;
         const long long t0 = clock64();
         const uint32_t c = A.proc_cell[w];
+        EIK_CHECK(c < A.cap, "round cell id");
         if (tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
         unsigned long long nsw = 0;
         cell_process<T, R>(A, S, Msm, c, A.proc_flags[w], nsw);
@@ -1141,6 +1163,7 @@ k_async(CellArgs A)
                     if (atomicCAS(&ctl->q_head, h, h + 1u) == h) {
                         uint32_t v;
                         while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) __nanosleep(20);
+                        EIK_CHECK(v < A.cap, "ring cell id");
                         // readiness (the heap order of Alg. 3 approximated locally): defer v
                         // while an adjacent cell is running or is queued with a smaller key
                         // (ties broken by index, so the minimum is never deferred)

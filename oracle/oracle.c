@@ -120,7 +120,8 @@ static int neighbours(const grid_t* g, int64_t p, int64_t nb[6])
 /* ---------------------------------------------------------------------------------------
  * Fast Marching Method.  Binary min-heap keyed on V, with a
  * back-pointer array for decrease-key.  Returns 0 on success, 1 if the accepted values were
- * ever decreasing (S:213 assertion), 2 on allocation failure, 3 if M >= 2^31.
+ * ever decreasing by more than rounding (S:213 assertion), 2 on allocation failure, 3 if
+ * M >= 2^31.
  * n_accepted (optional) receives the number of accepted points.
  * ------------------------------------------------------------------------------------- */
 enum { FAR = 0, TRIAL = 1, ACCEPTED = 2 };
@@ -206,8 +207,11 @@ int orc_fmm(int64_t n, double h, const double* F, const uint8_t* mask, const dou
         int32_t p = heap_pop(&hp);                       /* C.2 step 2 */
         state[p] = ACCEPTED;
         acc++;
-        if (V[p] < last) status = 1;
-        last = V[p];
+        /* pops are non-decreasing in exact arithmetic; at the switching tie of R4
+           (hf barely > a2 - a1) rounding can place a two-sided value an ulp below a2, so a
+           decrease is only an error beyond 64 ulp */
+        if (V[p] < last - 64.0 * 2.220446049250313e-16 * last) status = 1;
+        if (V[p] > last) last = V[p];
         int64_t nb[6];
         int c = neighbours(&g, p, nb);
         for (int e = 0; e < c; ++e) {                    /* C.2 step 3 */

@@ -35,6 +35,9 @@ WORKLOADS = {
     "C1": ("C1", "f64", 8), "C2": ("C2", "f32", 16), "C2d": ("C2", "f64", 8),
     "C3": ("C3", "f32", 16), "C3d": ("C3", "f64", 16), "C4": ("C4", "f32", 16),
     "C5": ("C5", "f32", 16),
+    # the paper's own suite, M = 320^3 / 352^3 as in P:837-906, fp64, r = 8
+    "P1": ("P1", "f64", 8), "P2": ("P2", "f64", 8), "P3": ("P3", "f64", 8),
+    "PCB11": ("PCB11", "f64", 8), "PMAZE": ("PMAZE", "f64", 8),
 }
 DESC = {
     "C1": "n=128 (129^3), F=1, centre exit",
@@ -42,7 +45,13 @@ DESC = {
     "C3": "n=512 (513^3), 8^3 checkerboard F in {1,10}, exit (0,0,0)",
     "C4": "n=512 (513^3), 8 F=0 walls with 4 random holes each, exit face z=0",
     "C5": "n=1024 (1025^3), 32 Gaussian bumps, 64 random exits",
+    "P1": "paper Ex.1, M=320^3, F=1, 8-point centre exit (P:760)",
+    "P2": "paper Ex.2, M=320^3, F=1+.5 sin(20pi x)sin(20pi y)sin(20pi z) (P:762)",
+    "P3": "paper Ex.3, M=320^3, F=1+.99 sin(2pi x)sin(2pi y)sin(2pi z) (P:764)",
+    "PCB11": "paper checkerboard K=11, M=352^3, F in {1,2} (P:1596)",
+    "PMAZE": "paper shell maze, M=320^3 on [-1,1]^3, F=.001 barriers (P:1627)",
 }
+PAPER_N = {"P1": 320, "P2": 320, "P3": 320, "PCB11": 352, "PMAZE": 320}
 
 
 def peaks():
@@ -111,10 +120,25 @@ def make_inputs(cfg, prec, device, n=None):
         m[idx] = 1
         q = torch.zeros((n + 1) ** 3, dtype=dt, device=device)
         return n, F.contiguous(), m, q
-    w = W.make(cfg, n)
+    w = paper_workload(cfg, n) if cfg in PAPER_N else W.make(cfg, n)
     Fh, mh, qh = w.as_dtype(np.float32 if prec == "f32" else np.float64)
     return (w.n, torch.from_numpy(Fh.reshape(-1)).to(device), torch.from_numpy(mh.reshape(-1)).to(device),
             torch.from_numpy(qh.reshape(-1)).to(device))
+
+
+def paper_workload(cfg, N=None):
+    import workloads as W
+    N = N or PAPER_N[cfg]
+    if cfg in ("P1", "P2", "P3"):
+        return W.paper_example(int(cfg[1]), N)
+    if cfg == "PCB11":
+        return W.paper_checkerboard(11, N)
+    return W.paper_shell_maze(N)
+
+
+def grid_h(cfg, n):
+    """grid spacing of a config (the shell maze lives on [-1, 1]^3)"""
+    return 2.0 / n if cfg == "PMAZE" else 1.0 / n
 
 
 def job_time(t_local: float, pg=None, device=None) -> float:
@@ -138,14 +162,19 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
 
 
+def sample_workload(cfg, n):
+    """the same workload's formulas at a reduced size (n intervals; paper configs: n points)"""
+    import workloads as W
+    return paper_workload(cfg, n + (n % 2)) if cfg in PAPER_N else W.make(cfg, n)
+
+
 def cpu_oracle_sample(cfg, n_sample):
     """Time the fp64 FMM oracle as it stands on the same workload's formulas at reduced n."""
     import oracle
-    import workloads as W
-    w = W.make(cfg, n_sample)
+    w = sample_workload(cfg, n_sample)
     oracle.build()
     t0 = time.perf_counter()
-    oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals)
+    oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals, h=w.h)
     dt = time.perf_counter() - t0
     return w.M, dt
 
@@ -157,13 +186,12 @@ def run_reference(args):
     cfg, prec, r = WORKLOADS[args.config]
     n_s = args.ref_n
     import oracle
-    import workloads as W
     oracle.build()
-    w = W.make(cfg, n_s)
+    w = sample_workload(cfg, n_s)
     times = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals)
+        oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals, h=w.h)
         if s >= args.warmup:
             times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
@@ -181,7 +209,7 @@ def run_reference(args):
 
 
 def config_block(cfg, prec, r, n=None):
-    n = n or {"C1": 128, "C2": 256, "C3": 512, "C4": 512, "C5": 1024}[cfg]
+    n = n or {"C1": 128, "C2": 256, "C3": 512, "C4": 512, "C5": 1024}.get(cfg) or PAPER_N[cfg] - 1
     return {"workload": f"{cfg}: {DESC[cfg]}", "n": n, "points": (n + 1) ** 3, "cell_size": r,
             "precision": prec, "solve": "eik_solve: ingest + device scheduler loop + egress",
             "l2": "inputs (F + exit_mask + exit_vals) and tiles are > 4x the 126 MB L2; no flush"
@@ -231,7 +259,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
-        solver.solve(F, m, q, cell_size=r, n=n, out=U)
+        solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
@@ -239,7 +267,7 @@ def main():
     with Clocks(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            solver.solve(F, m, q, cell_size=r, n=n, out=U)
+            solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
             stats.append(solver.stats())
         ev1.record(stream)
         barrier()
@@ -256,7 +284,7 @@ def main():
     # event-timed cross-check of the same kernel (host-loop mode, CUDA events around launches)
     s2 = eik.Solver(device=local, loop_mode=1, bin_width=args.bin_width)
     s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
-    s2.solve(F, m, q, cell_size=r, n=n, out=torch.empty_like(F))
+    s2.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=torch.empty_like(F))
     st2 = s2.stats()
     s2.close()
     traffic = None
@@ -281,11 +309,11 @@ def main():
         mh = m.cpu().pin_memory()
         qh = q.cpu().pin_memory()
         Uh = torch.empty_like(Fh).pin_memory()
-        solver.solve_host(Fh, mh, qh, cell_size=r, n=n, out=Uh)
+        solver.solve_host(Fh, mh, qh, h=grid_h(cfg, n), cell_size=r, n=n, out=Uh)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            solver.solve_host(Fh, mh, qh, cell_size=r, n=n, out=Uh)
+            solver.solve_host(Fh, mh, qh, h=grid_h(cfg, n), cell_size=r, n=n, out=Uh)
         t_e = job_time((time.perf_counter() - t0) / args.e2e_steps, pg, dev)
         e2e = {"value": job_value(M, ws, t_e), "unit": UNIT, "ms_per_step": t_e * 1e3,
                "h2d_bytes_per_step": int(Fh.numel() * Fh.element_size() + mh.numel() + qh.numel() * qh.element_size()),

@@ -53,7 +53,7 @@ class Workload:
 
     @property
     def h(self) -> float:
-        return 1.0 / self.n
+        return float(self.meta.get("h", 1.0 / self.n))
 
     @property
     def M(self) -> int:
@@ -219,3 +219,68 @@ def random_instance(n: int, seed: int, p_wall: float = 0.15, n_exits: int = 3,
     if q_max > 0:
         q.reshape(-1)[flat] = rng.uniform(0.0, q_max, n_exits)
     return Workload(f"rand{n}_{seed}", n, F, mask, q, dict(seed=seed))
+
+
+# --------------------------------------------------------------------------------------
+# The paper's own workload suite: M = N^3 points per side N on the unit
+# cube (h = 1/(N-1)); N even, so the exit set is the 8 gridpoints closest to the centre
+# ("we have initialized U on the set Q of the 8 gridpoints closest to the center").
+# --------------------------------------------------------------------------------------
+def _centre8(N: int):
+    assert N % 2 == 0, "the paper's centre-exit problems use an even number of points per side"
+    lo, hi = N // 2 - 1, N // 2
+    return [(i, j, k) for i in (lo, hi) for j in (lo, hi) for k in (lo, hi)]
+
+
+def paper_example(ex: int, N: int) -> Workload:
+    """Examples 1-3 of P:760-764 on N^3 points: F = 1; 1 + .5 sin(20 pi x) sin(20 pi y)
+    sin(20 pi z); 1 + .99 sin(2 pi x) sin(2 pi y) sin(2 pi z); q = 0 on the 8 centre points."""
+    n = N - 1
+    x = np.arange(N, dtype=np.float64) / n
+    if ex == 1:
+        F = np.ones((N,) * 3)
+    else:
+        a, w = (0.5, 20.0) if ex == 2 else (0.99, 2.0)
+        sv = np.sin(w * np.pi * x)
+        F = 1.0 + a * (sv[:, None, None] * sv[None, :, None] * sv[None, None, :])
+    mask, q = _point_exits(n, _centre8(N))
+    return Workload(f"Ex{ex}_{N}", n, np.ascontiguousarray(F), mask, q, dict(ex=ex, N=N))
+
+
+def paper_checkerboard(K: int, N: int) -> Workload:
+    """3D checkerboard of P:1596-1600: K^3 checkers of edge 1/K, F = 2 on black and 1 on white
+    checkers, centre exit (8 points).  Reading: black = checkers with odd bx+by+bz (the centre
+    checker for odd K); a gridpoint on a checker boundary takes the checker floor(x K) (the
+    paper picks grids avoiding this, P:1597 footnote)."""
+    n = N - 1
+    x = np.arange(N, dtype=np.float64) / n
+    b = np.minimum(np.floor(x * K).astype(np.int64), K - 1)
+    par = (b[:, None, None] + b[None, :, None] + b[None, None, :]) % 2
+    F = np.where(par == 1, 2.0, 1.0)
+    mask, q = _point_exits(n, _centre8(N))
+    return Workload(f"CB{K}_{N}", n, np.ascontiguousarray(F), mask, q, dict(K=K, N=N))
+
+
+def paper_shell_maze(N: int, t: float = 1.0 / 12, w: float = 0.1, slow: float = 0.001) -> Workload:
+    """Permeable spherical-shell maze of P:1627-1636 on [-1,1]^3 (h = 2/(N-1)): F = 1 outside
+    four barriers A_1..A_4 (radii .3/.5/.7/.9, thickness t, openings x^2 + y^2 < w on
+    alternating sides z < 0 / z > 0) and F = .001 inside them; exits at the gridpoint(s)
+    closest to the origin (8 for even N)."""
+    n = N - 1
+    x = -1.0 + 2.0 * np.arange(N, dtype=np.float64) / n
+    X = x[None, None, :]
+    Y = x[None, :, None]
+    Z = x[:, None, None]
+    rad = np.sqrt(X * X + Y * Y + Z * Z)
+    hole = (X * X + Y * Y) < w
+    F = np.ones((N,) * 3)
+    for r0, neg in ((0.3, True), (0.5, False), (0.7, True), (0.9, False)):
+        shell = (rad > r0) & (rad < r0 + t)
+        opening = hole & ((Z < 0) if neg else (Z > 0))
+        F[shell & ~opening] = slow
+    if N % 2 == 0:
+        ex = _centre8(N)
+    else:
+        ex = [(n // 2,) * 3]
+    mask, q = _point_exits(n, ex)
+    return Workload(f"Maze_{N}", n, np.ascontiguousarray(F), mask, q, dict(N=N, h=2.0 / n))

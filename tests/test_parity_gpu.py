@@ -209,3 +209,35 @@ def test_full_c2_all_variants(solver):
     for dt in (np.float64, np.float32):
         for r in (8, 16):
             assert_parity(_gpu(solver, w, dt, r), U_orc, w, dt)
+
+
+def test_watchdog_turns_a_long_loop_into_an_error():
+    """EIK_OPT_TIMEOUT_S: the device loop stops, the call returns EIK_EINTERNAL, and the same
+    context solves correctly afterwards (round and async modes)."""
+    import paper_1306_4743_b200 as eik
+    w = W.c2(64)
+    for mode in (2, 0):
+        s = eik.Solver(device=0, loop_mode=mode)
+        s.set_option(eik.EIK_OPT_TIMEOUT_S, 1e-6)
+        with pytest.raises(eik.EikError) as ei:
+            _gpu(s, w, np.float64, 8)
+        assert ei.value.status == eik.EIK_EINTERNAL
+        s.set_option(eik.EIK_OPT_TIMEOUT_S, 60)
+        assert_parity(_gpu(s, w, np.float64, 8), oracle_U(w), w, np.float64)
+        s.close()
+
+
+def test_solve_on_a_side_stream():
+    """The solve is enqueued on torch's current stream (a non-default one here)."""
+    import torch
+    import paper_1306_4743_b200 as eik
+    w = W.c3(32)
+    F, m, q = w.as_dtype(np.float32)
+    s = eik.Solver(device=0)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        tF, tm, tq = (torch.from_numpy(a).cuda() for a in (F, m, q))
+        U = s.solve(tF, tm, tq, cell_size=16, n=w.n)
+    st.synchronize()
+    assert_parity(U.cpu().numpy(), oracle_U(w), w, np.float32)
+    s.close()

@@ -861,6 +861,49 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             }                                                                              \
         }
         EIK_PREFETCH(s)
+        // First sweep of a cell with many active points (a fresh cell the front is entering):
+        // relax every point of every plane without per-point gating -- nearly all of them
+        // change anyway -- and record only the activations *behind* the wavefront, which the
+        // next sweep needs (forward neighbours are visited later in this same sweep).
+        const bool ungated = first && nact >= R3 / 8;
+        if (ungated) {
+            for (; s < NPL; ++s) {
+                const int e = en;
+                const T hs = hn;
+                EIK_PREFETCH(s + 1)
+                if (e >= 0) {
+                    const unsigned ue = (unsigned)e;
+                    const int p = (int)(ue ^ dm);
+                    EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
+                    sA[p] = 0;                                             // Alg. 2 line 4
+                    const unsigned up = (unsigned)p;
+                    const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
+                    const T v = sV[q];
+                    const T xf = sV[q + oxq], xb = sV[q - oxq];
+                    const T yf = sV[q + oyq], yb = sV[q - oyq];
+                    const T zf = sV[q + ozq], zb = sV[q - ozq];
+                    const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
+                    const T hf = fabs(hs);
+                    if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
+                        ++nupd;
+                        const T u = local_solve_fast<T>(mx, my, mz, hf);
+                        if (u < v) {
+                            sV[q] = u;
+                            if (hs > T(0)) sH[p] = -hs;
+                            ++nwr;
+                            const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
+                            const int bxa = (xb > u) & (ca > 0), bya = (yb > u) & (cb > 0), bza = (zb > u) & (cc > 0);
+                            sA[bxa ? p - oxp : R3] = 1;
+                            sA[bya ? p - oyp : R3] = 1;
+                            sA[bza ? p - ozp : R3] = 1;
+                            bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
+                        }
+                    }
+                }
+                __syncthreads();
+                ++nsteps;
+            }
+        }
         for (; s < NPL; ++s) {
             const bool has = (pm >> s) & 1ull;
             if (!has && !fwd) {

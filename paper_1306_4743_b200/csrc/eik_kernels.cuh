@@ -472,6 +472,148 @@ __device__ __forceinline__ void cell_init_tables(const CellArgs& A, CellShared<R
     for (int e = threadIdx.x; e < C::R3; e += C::NT) M.tab[e] = __ldg(&A.plane_tab[e]);
 }
 
+// One wavefront sweep in the compile-time direction DIR (bit0/1/2 = x/y/z descending): the
+// direction's reflection mask and neighbour offsets are immediates.  Returns the axes along
+// which points behind the wavefront were activated (bit0 x, bit1 y, bit2 z).
+template <typename T, int R, int DIR>
+__device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& M,
+                                              unsigned long long pm, bool ungated,
+                                              uint32_t& nupd, uint32_t& nwr, uint32_t& nsteps)
+{
+    using C = CellCfg<R>;
+    constexpr int R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
+    constexpr bool fx = DIR & 1, fy = DIR & 2, fz = DIR & 4;
+    const int tid = threadIdx.x;
+    T* sV = M.V;
+    T* sH = M.H;
+    uint8_t* sA = M.act;
+    const T INF = dinf<T>();
+        bool fwd = false;
+    uint32_t bwd = 0;
+    int s = __ffsll((long long)pm) - 1;
+    // The plane table holds canonical (reflected) coordinates e = a + R b + R^2 c with
+    // a + b + c = s.  The point index is p = e XOR dm (R a power of two: reflecting an axis
+    // XORs its field); in canonical coordinates "forward" along an axis is +1 and the
+    // forward / backward neighbours exist iff the coordinate is < R-1 / > 0.  Box and flag
+    // offsets of the forward neighbours are per-sweep constants.
+    constexpr unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
+    constexpr int oxq = fx ? -1 : 1, oyq = fy ? -RP : RP, ozq = fz ? -RP2 : RP2;   // box
+    constexpr int oxp = fx ? -1 : 1, oyp = fy ? -R : R, ozp = fz ? -R * R : R * R;  // flags
+    // prefetch: the canonical entry this thread owns at plane sp and its hf
+    int en = -1;
+    T hn = INF;
+#define EIK_PREFETCH(sp_)                                                                  \
+    {                                                                                  \
+        const int sp = (sp_);                                                          \
+        en = -1;                                                                       \
+        if (sp < NPL) {                                                                \
+            const int e_ = S.off[sp] + tid;                                            \
+            if (e_ < S.off[sp + 1]) { en = M.tab[e_]; hn = sH[en ^ dm]; }              \
+        }                                                                              \
+    }
+    EIK_PREFETCH(s)
+    // First sweep of a cell with many active points (a fresh cell the front is entering):
+    // relax every point of every plane without per-point gating -- nearly all of them
+    // change anyway -- and record only the activations *behind* the wavefront, which the
+    // next sweep needs (forward neighbours are visited later in this same sweep).
+    if (ungated) {
+        for (; s < NPL; ++s) {
+            const int e = en;
+            const T hs = hn;
+            EIK_PREFETCH(s + 1)
+            if (e >= 0) {
+                const unsigned ue = (unsigned)e;
+                const int p = (int)(ue ^ dm);
+                EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
+                sA[p] = 0;                                             // Alg. 2 line 4
+                const unsigned up = (unsigned)p;
+                const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
+                const T v = sV[q];
+                const T xf = sV[q + oxq], xb = sV[q - oxq];
+                const T yf = sV[q + oyq], yb = sV[q - oyq];
+                const T zf = sV[q + ozq], zb = sV[q - ozq];
+                const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
+                const T hf = fabs(hs);
+                if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
+                    ++nupd;
+                    const T u = local_solve_fast<T>(mx, my, mz, hf);
+                    if (u < v) {
+                        sV[q] = u;
+                        if (hs > T(0)) sH[p] = -hs;
+                        ++nwr;
+                        const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
+                        const int bxa = (xb > u) & (ca > 0), bya = (yb > u) & (cb > 0), bza = (zb > u) & (cc > 0);
+                        sA[bxa ? p - oxp : R3] = 1;
+                        sA[bya ? p - oyp : R3] = 1;
+                        sA[bza ? p - ozp : R3] = 1;
+                        bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
+                    }
+                }
+            }
+            __syncthreads();
+            ++nsteps;
+        }
+    }
+    for (; s < NPL; ++s) {
+        const bool has = (pm >> s) & 1ull;
+        if (!has && !fwd) {
+            if ((pm >> s) == 0ull) break;
+            EIK_PREFETCH(s + 1)
+            continue;
+        }
+        const int e = en;
+        const T hs = hn;
+        EIK_PREFETCH(s + 1)   // independent of this step's results
+        bool myfwd = false;
+        if (e >= 0) {
+            const unsigned ue = (unsigned)e;
+            const int p = (int)(ue ^ dm);
+            EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
+            if (sA[p]) {
+                sA[p] = 0;                                             // Alg. 2 line 4
+                const unsigned up = (unsigned)p;
+                const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
+                EIK_CHECK(q - RP2 >= 0 && q + RP2 < C::BOX, "box index");
+                const T v = sV[q];
+                const T xf = sV[q + oxq], xb = sV[q - oxq];
+                const T yf = sV[q + oyq], yb = sV[q - oyq];
+                const T zf = sV[q + ozq], zb = sV[q - ozq];
+                const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
+                const T hf = fabs(hs);
+                if (hf < INF && fmin(mx, fmin(my, mz)) < v) {          // fixed / no gain
+                    ++nupd;
+                    const T u = local_solve_fast<T>(mx, my, mz, hf);    // line 5
+                    if (u < v) {                                         // line 6
+                        sV[q] = u;                                       // line 7
+                        if (hs > T(0)) sH[p] = -hs;                      // mark changed
+                        ++nwr;
+                        // lines 8-13: activate larger in-cell neighbours (the cross-border
+                        // "currently downwind" test is done once per processing)
+                        const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
+                        // activations as unconditional byte stores to either the neighbour
+                        // or a scratch byte (short-lived compares, no predicate pressure)
+                        const int fxa = (xf > u) & (ca < R - 1), bxa = (xb > u) & (ca > 0);
+                        const int fya = (yf > u) & (cb < R - 1), bya = (yb > u) & (cb > 0);
+                        const int fza = (zf > u) & (cc < R - 1), bza = (zb > u) & (cc > 0);
+                        sA[fxa ? p + oxp : R3] = 1;
+                        sA[bxa ? p - oxp : R3] = 1;
+                        sA[fya ? p + oyp : R3] = 1;
+                        sA[bya ? p - oyp : R3] = 1;
+                        sA[fza ? p + ozp : R3] = 1;
+                        sA[bza ? p - ozp : R3] = 1;
+                        myfwd = (fxa | fya | fza) != 0;
+                        bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
+                    }
+                }
+            }
+        }
+        fwd = __syncthreads_or(myfwd);
+        ++nsteps;
+    }
+#undef EIK_PREFETCH
+    return bwd;
+}
+
 // Process one cell to convergence (HCM "perform modified LSM on c until convergence",
 // Alg. 1 line 6): stage the tile and its one-point halo N(c) (boundary data of
 // c~ = c u N(c)), relax the gated (LSM) update of Alg. 2 until no point is active, write
@@ -502,7 +644,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 {
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
-    constexpr int LCAP = C::LCAP, PPT = C::PPT;
+    constexpr int LCAP = C::LCAP;
     const int tid = threadIdx.x;
     T* Vt = reinterpret_cast<T*>(A.Vt);
     const T* Ht = reinterpret_cast<const T*>(A.Ht);
@@ -837,130 +979,20 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             break;
         }
         ++nsweeps;
-        bool fwd = false;
         uint32_t bwd = 0;
-        int s = __ffsll((long long)pm) - 1;
-        // The plane table holds canonical (reflected) coordinates e = a + R b + R^2 c with
-        // a + b + c = s.  The point index is p = e XOR dm (R a power of two: reflecting an axis
-        // XORs its field); in canonical coordinates "forward" along an axis is +1 and the
-        // forward / backward neighbours exist iff the coordinate is < R-1 / > 0.  Box and flag
-        // offsets of the forward neighbours are per-sweep constants.
-        const unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
-        const int oxq = fx ? -1 : 1, oyq = fy ? -RP : RP, ozq = fz ? -RP2 : RP2;   // box
-        const int oxp = fx ? -1 : 1, oyp = fy ? -R : R, ozp = fz ? -R * R : R * R;  // flags
-        // prefetch: the canonical entry this thread owns at plane sp and its hf
-        int en = -1;
-        T hn = INF;
-#define EIK_PREFETCH(sp_)                                                                  \
-        {                                                                                  \
-            const int sp = (sp_);                                                          \
-            en = -1;                                                                       \
-            if (sp < NPL) {                                                                \
-                const int e_ = S.off[sp] + tid;                                            \
-                if (e_ < S.off[sp + 1]) { en = M.tab[e_]; hn = sH[en ^ dm]; }              \
-            }                                                                              \
-        }
-        EIK_PREFETCH(s)
-        // First sweep of a cell with many active points (a fresh cell the front is entering):
-        // relax every point of every plane without per-point gating -- nearly all of them
-        // change anyway -- and record only the activations *behind* the wavefront, which the
-        // next sweep needs (forward neighbours are visited later in this same sweep).
-        const bool ungated = first && nact >= R3 / 8;
-        if (ungated) {
-            for (; s < NPL; ++s) {
-                const int e = en;
-                const T hs = hn;
-                EIK_PREFETCH(s + 1)
-                if (e >= 0) {
-                    const unsigned ue = (unsigned)e;
-                    const int p = (int)(ue ^ dm);
-                    EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
-                    sA[p] = 0;                                             // Alg. 2 line 4
-                    const unsigned up = (unsigned)p;
-                    const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
-                    const T v = sV[q];
-                    const T xf = sV[q + oxq], xb = sV[q - oxq];
-                    const T yf = sV[q + oyq], yb = sV[q - oyq];
-                    const T zf = sV[q + ozq], zb = sV[q - ozq];
-                    const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
-                    const T hf = fabs(hs);
-                    if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
-                        ++nupd;
-                        const T u = local_solve_fast<T>(mx, my, mz, hf);
-                        if (u < v) {
-                            sV[q] = u;
-                            if (hs > T(0)) sH[p] = -hs;
-                            ++nwr;
-                            const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
-                            const int bxa = (xb > u) & (ca > 0), bya = (yb > u) & (cb > 0), bza = (zb > u) & (cc > 0);
-                            sA[bxa ? p - oxp : R3] = 1;
-                            sA[bya ? p - oyp : R3] = 1;
-                            sA[bza ? p - ozp : R3] = 1;
-                            bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
-                        }
-                    }
-                }
-                __syncthreads();
-                ++nsteps;
+        {
+            const bool ungated = first && nact >= R3 / 8;
+            switch (dir) {
+            case 0: bwd = sweep_dir<T, R, 0>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 1: bwd = sweep_dir<T, R, 1>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 2: bwd = sweep_dir<T, R, 2>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 3: bwd = sweep_dir<T, R, 3>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 4: bwd = sweep_dir<T, R, 4>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 5: bwd = sweep_dir<T, R, 5>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 6: bwd = sweep_dir<T, R, 6>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            default: bwd = sweep_dir<T, R, 7>(S, M, pm, ungated, nupd, nwr, nsteps); break;
             }
         }
-        for (; s < NPL; ++s) {
-            const bool has = (pm >> s) & 1ull;
-            if (!has && !fwd) {
-                if ((pm >> s) == 0ull) break;
-                EIK_PREFETCH(s + 1)
-                continue;
-            }
-            const int e = en;
-            const T hs = hn;
-            EIK_PREFETCH(s + 1)   // independent of this step's results
-            bool myfwd = false;
-            if (e >= 0) {
-                const unsigned ue = (unsigned)e;
-                const int p = (int)(ue ^ dm);
-                EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
-                if (sA[p]) {
-                    sA[p] = 0;                                             // Alg. 2 line 4
-                    const unsigned up = (unsigned)p;
-                    const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
-                    EIK_CHECK(q - RP2 >= 0 && q + RP2 < C::BOX, "box index");
-                    const T v = sV[q];
-                    const T xf = sV[q + oxq], xb = sV[q - oxq];
-                    const T yf = sV[q + oyq], yb = sV[q - oyq];
-                    const T zf = sV[q + ozq], zb = sV[q - ozq];
-                    const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
-                    const T hf = fabs(hs);
-                    if (hf < INF && fmin(mx, fmin(my, mz)) < v) {          // fixed / no gain
-                        ++nupd;
-                        const T u = local_solve_fast<T>(mx, my, mz, hf);    // line 5
-                        if (u < v) {                                         // line 6
-                            sV[q] = u;                                       // line 7
-                            if (hs > T(0)) sH[p] = -hs;                      // mark changed
-                            ++nwr;
-                            // lines 8-13: activate larger in-cell neighbours (the cross-border
-                            // "currently downwind" test is done once per processing)
-                            const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
-                            // activations as unconditional byte stores to either the neighbour
-                            // or a scratch byte (short-lived compares, no predicate pressure)
-                            const int fxa = (xf > u) & (ca < R - 1), bxa = (xb > u) & (ca > 0);
-                            const int fya = (yf > u) & (cb < R - 1), bya = (yb > u) & (cb > 0);
-                            const int fza = (zf > u) & (cc < R - 1), bza = (zb > u) & (cc > 0);
-                            sA[fxa ? p + oxp : R3] = 1;
-                            sA[bxa ? p - oxp : R3] = 1;
-                            sA[fya ? p + oyp : R3] = 1;
-                            sA[bya ? p - oyp : R3] = 1;
-                            sA[fza ? p + ozp : R3] = 1;
-                            sA[bza ? p - ozp : R3] = 1;
-                            myfwd = (fxa | fya | fza) != 0;
-                            bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
-                        }
-                    }
-                }
-            }
-            fwd = __syncthreads_or(myfwd);
-            ++nsteps;
-        }
-#undef EIK_PREFETCH
         tstep += clock64() - tm1;
         nact = LCAP + 1;   // unknown until the next scan
         for (int o = 16; o > 0; o >>= 1) bwd |= __shfl_xor_sync(0xffffffffu, bwd, o);

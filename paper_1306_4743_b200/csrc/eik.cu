@@ -55,7 +55,6 @@ struct eik_ctx {
     Ctl* ctl_host = nullptr;      // pinned
     // plane tables per r (index 0: r=4, 1: r=8, 2: r=16)
     uint16_t* plane_tab[3] = {nullptr, nullptr, nullptr};
-    int32_t* plane_off[3] = {nullptr, nullptr, nullptr};
     // host-pointer staging (eik_solve_host)
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -94,22 +93,24 @@ static int fail(eik_ctx* ctx, int code, const char* fmt, ...)
 
 static int rindex_of(int r) { return r == 4 ? 0 : r == 8 ? 1 : r == 16 ? 2 : -1; }
 
-// wavefront plane table for an r^3 cell: canonical point indices a + r b + r^2 c sorted by
-// plane a+b+c (a direction's table is this one XOR the reflection mask, r a power of two)
-static void make_plane_table(int r, std::vector<uint16_t>& tab, std::vector<int32_t>& off)
+// wavefront plane table for an r^3 cell, indexed [plane s][thread t]: the canonical point
+// index a + r b + r^2 c of the t-th point (a, b, c) of plane a+b+c = s, or 0xFFFF when plane s
+// has <= t points.  Two trailing all-empty planes let the sweep prefetch two planes ahead
+// without a bounds test.  A direction's point is this entry XOR its reflection mask (r a power
+// of two).  nt = threads of the cell kernel (CellCfg<r>::NT >= the largest plane).
+static void make_plane_table(int r, int nt, std::vector<uint16_t>& tab)
 {
     const int npl = 3 * r - 2;
-    tab.clear();
-    off.assign(npl + 1, 0);
+    tab.assign((size_t)(npl + 2) * nt, (uint16_t)0xFFFF);
     for (int s = 0; s < npl; ++s) {
-        off[s] = (int32_t)tab.size();
+        int t = 0;
         for (int c = 0; c < r; ++c)
             for (int b = 0; b < r; ++b) {
                 const int a = s - b - c;
-                if (a >= 0 && a < r) tab.push_back((uint16_t)(a + r * b + r * r * c));   // canonical p
+                if (a >= 0 && a < r) tab[(size_t)s * nt + t++] = (uint16_t)(a + r * b + r * r * c);
             }
+        if (t > nt) std::abort();   // CellCfg<r>::NT smaller than a plane: programming error
     }
-    off[npl] = (int32_t)tab.size();
 }
 
 extern "C" int eik_abi_version(void) { return EIK_ABI_VERSION; }
@@ -145,14 +146,12 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&ctx->ev[i]));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreate(&ctx->cev[i]));
     const int rs[3] = {4, 8, 16};
+    const int nts[3] = {CellCfg<4>::NT, CellCfg<8>::NT, CellCfg<16>::NT};
     for (int t = 0; t < 3; ++t) {
         std::vector<uint16_t> tab;
-        std::vector<int32_t> off;
-        make_plane_table(rs[t], tab, off);
+        make_plane_table(rs[t], nts[t], tab);
         CK(cudaMalloc(&ctx->plane_tab[t], tab.size() * sizeof(uint16_t)));
-        CK(cudaMalloc(&ctx->plane_off[t], off.size() * sizeof(int32_t)));
         CK(cudaMemcpy(ctx->plane_tab[t], tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(ctx->plane_off[t], off.data(), off.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     // opt in to > 48 KB dynamic shared memory for the cell kernels
     CK(cudaFuncSetAttribute(k_cell<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
@@ -193,7 +192,7 @@ extern "C" void eik_destroy(eik_ctx* ctx)
     cudaFree(ctx->stage);
     cudaFree(ctx->ctl);
     cudaFreeHost(ctx->ctl_host);
-    for (int t = 0; t < 3; ++t) { cudaFree(ctx->plane_tab[t]); cudaFree(ctx->plane_off[t]); }
+    for (int t = 0; t < 3; ++t) cudaFree(ctx->plane_tab[t]);
     for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
     for (int i = 0; i < 2; ++i) if (ctx->cev[i]) cudaEventDestroy(ctx->cev[i]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -513,7 +512,6 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.state = ctx->state;
     const int ri = rindex_of(r);
     ca.plane_tab = ctx->plane_tab[ri];
-    ca.plane_off = ctx->plane_off[ri];
     ca.Vt = ctx->Vt;
     ca.Ht = ctx->Ht;
     ca.max_sweeps = ctx->max_sweeps;

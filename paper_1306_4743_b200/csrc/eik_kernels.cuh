@@ -381,8 +381,8 @@ template <> struct MinBlocks<double, 16> { static constexpr int value = 2; };
 template <typename T, int R>
 constexpr size_t cell_smem_bytes()
 {
-    // V box + hf + plane table (uint16) + active bytes + 2 active lists (uint16)
-    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + 3 * CellCfg<R>::R3 + 16 + 4 * CellCfg<R>::LCAP;
+    // V box + hf + active bytes (+ scratch) + 2 active lists (uint16)
+    return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + CellCfg<R>::R3 + 16 + 4 * CellCfg<R>::LCAP;
 }
 
 struct CellArgs {
@@ -395,8 +395,7 @@ struct CellArgs {
     uint32_t* key;
     uint32_t* state;
     uint32_t* gen;               // async mode: BFS generation of each cell (readiness mode 5)
-    const uint16_t* plane_tab;   // R^3 entries (a | b<<4 | c<<8) sorted by plane a+b+c
-    const int32_t* plane_off;    // NPL + 1 offsets
+    const uint16_t* plane_tab;   // [NPL + 2][NT] canonical point of thread t in plane s (0xFFFF: none)
     void* Vt;
     const void* Ht;
     int64_t n1;
@@ -432,7 +431,6 @@ template <> struct Vec16<double> { using type = double2; };
 
 // Shared-memory state of one cell processing (static part; the big arrays are dynamic).
 template <int R> struct CellShared {
-    int32_t off[CellCfg<R>::NPL + 1];  // plane offsets into the plane table
     unsigned long long plane[2];
     uint32_t face_min[6];              // Eq. (3) min newly-updated inflow value per face
     uint32_t face_flag;                // faces whose neighbour is currently downwind
@@ -450,33 +448,23 @@ template <int R> struct CellShared {
 template <typename T, int R> struct CellSmem {
     T* V;          // (R+2)^3 box incl. halo faces
     T* H;          // R^3 hf (sign bit set = point changed in this processing)
-    uint16_t* tab; // plane table
     uint8_t* act;  // R^3 active flags (Alg. 2)
     uint16_t* list; // 2 x LCAP active-point lists
     __device__ explicit CellSmem(unsigned char* raw)
     {
         V = reinterpret_cast<T*>(raw);
         H = V + CellCfg<R>::BOX;
-        tab = reinterpret_cast<uint16_t*>(H + CellCfg<R>::R3);
-        act = reinterpret_cast<uint8_t*>(tab + CellCfg<R>::R3);
+        act = reinterpret_cast<uint8_t*>(H + CellCfg<R>::R3);
         list = reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3 + 16);   // act[R3] = scratch
     }
 };
-
-// once per CTA: plane table and offsets into shared memory
-template <typename T, int R>
-__device__ __forceinline__ void cell_init_tables(const CellArgs& A, CellShared<R>& S, CellSmem<T, R>& M)
-{
-    using C = CellCfg<R>;
-    for (int s = threadIdx.x; s <= C::NPL; s += C::NT) S.off[s] = __ldg(&A.plane_off[s]);
-    for (int e = threadIdx.x; e < C::R3; e += C::NT) M.tab[e] = __ldg(&A.plane_tab[e]);
-}
 
 // One wavefront sweep in the compile-time direction DIR (bit0/1/2 = x/y/z descending): the
 // direction's reflection mask and neighbour offsets are immediates.  Returns the axes along
 // which points behind the wavefront were activated (bit0 x, bit1 y, bit2 z).
 template <typename T, int R, int DIR>
 __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& M,
+                                              const uint16_t* __restrict__ ptab,
                                               unsigned long long pm, bool ungated,
                                               uint32_t& nupd, uint32_t& nwr, uint32_t& nsteps)
 {
@@ -488,7 +476,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     T* sH = M.H;
     uint8_t* sA = M.act;
     const T INF = dinf<T>();
-        bool fwd = false;
+    bool fwd = false;
     uint32_t bwd = 0;
     int s = __ffsll((long long)pm) - 1;
     // The plane table holds canonical (reflected) coordinates e = a + R b + R^2 c with
@@ -499,30 +487,31 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     constexpr unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
     constexpr int oxq = fx ? -1 : 1, oyq = fy ? -RP : RP, ozq = fz ? -RP2 : RP2;   // box
     constexpr int oxp = fx ? -1 : 1, oyp = fy ? -R : R, ozp = fz ? -R * R : R * R;  // flags
-    // prefetch: the canonical entry this thread owns at plane sp and its hf
-    int en = -1;
-    T hn = INF;
+    // Two-stage prefetch, independent of the current step's results: at step s the thread
+    // holds its entry en / hf hn of plane s and the entry en1 of plane s + 1; the step loads
+    // hf of plane s + 1 (shared memory) and the entry of plane s + 2 (global table via L1),
+    // so no load sits on the step's critical path.  The table has two empty trailing planes.
+    const uint16_t* tp = ptab + tid;
+    constexpr int NT = C::NT;
+    unsigned en = __ldg(&tp[s * NT]);
+    unsigned en1 = __ldg(&tp[(s + 1) * NT]);
+    T hn = en < (unsigned)R3 ? sH[en ^ dm] : INF;
 #define EIK_PREFETCH(sp_)                                                                  \
     {                                                                                  \
-        const int sp = (sp_);                                                          \
-        en = -1;                                                                       \
-        if (sp < NPL) {                                                                \
-            const int e_ = S.off[sp] + tid;                                            \
-            if (e_ < S.off[sp + 1]) { en = M.tab[e_]; hn = sH[en ^ dm]; }              \
-        }                                                                              \
+        en = en1;                                                                      \
+        hn = en < (unsigned)R3 ? sH[en ^ dm] : INF;                                    \
+        en1 = __ldg(&tp[((sp_) + 1) * NT]);                                            \
     }
-    EIK_PREFETCH(s)
     // First sweep of a cell with many active points (a fresh cell the front is entering):
     // relax every point of every plane without per-point gating -- nearly all of them
     // change anyway -- and record only the activations *behind* the wavefront, which the
     // next sweep needs (forward neighbours are visited later in this same sweep).
     if (ungated) {
         for (; s < NPL; ++s) {
-            const int e = en;
+            const unsigned ue = en;
             const T hs = hn;
             EIK_PREFETCH(s + 1)
-            if (e >= 0) {
-                const unsigned ue = (unsigned)e;
+            if (ue < (unsigned)R3) {
                 const int p = (int)(ue ^ dm);
                 EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
                 sA[p] = 0;                                             // Alg. 2 line 4
@@ -561,12 +550,11 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
             EIK_PREFETCH(s + 1)
             continue;
         }
-        const int e = en;
+        const unsigned ue = en;
         const T hs = hn;
         EIK_PREFETCH(s + 1)   // independent of this step's results
         bool myfwd = false;
-        if (e >= 0) {
-            const unsigned ue = (unsigned)e;
+        if (ue < (unsigned)R3) {
             const int p = (int)(ue ^ dm);
             EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
             if (sA[p]) {
@@ -983,14 +971,14 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         {
             const bool ungated = first && nact >= R3 / 8;
             switch (dir) {
-            case 0: bwd = sweep_dir<T, R, 0>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            case 1: bwd = sweep_dir<T, R, 1>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            case 2: bwd = sweep_dir<T, R, 2>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            case 3: bwd = sweep_dir<T, R, 3>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            case 4: bwd = sweep_dir<T, R, 4>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            case 5: bwd = sweep_dir<T, R, 5>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            case 6: bwd = sweep_dir<T, R, 6>(S, M, pm, ungated, nupd, nwr, nsteps); break;
-            default: bwd = sweep_dir<T, R, 7>(S, M, pm, ungated, nupd, nwr, nsteps); break;
+            case 0: bwd = sweep_dir<T, R, 0>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 1: bwd = sweep_dir<T, R, 1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 2: bwd = sweep_dir<T, R, 2>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 3: bwd = sweep_dir<T, R, 3>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 4: bwd = sweep_dir<T, R, 4>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 5: bwd = sweep_dir<T, R, 5>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 6: bwd = sweep_dir<T, R, 6>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            default: bwd = sweep_dir<T, R, 7>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
             }
         }
         tstep += clock64() - tm1;
@@ -1133,7 +1121,6 @@ k_cell(CellArgs A)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CellSmem<T, R> Msm(smem_raw);
     __shared__ CellShared<R> S;
-    cell_init_tables<T, R>(A, S, Msm);
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
     const uint32_t nproc = ctl->proc_count;
@@ -1217,7 +1204,6 @@ k_async(CellArgs A)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CellSmem<T, R> Msm(smem_raw);
     __shared__ CellShared<R> S;
-    cell_init_tables<T, R>(A, S, Msm);
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
     uint32_t* ring = A.wl0;

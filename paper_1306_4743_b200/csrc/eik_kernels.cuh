@@ -54,6 +54,39 @@ __device__ __forceinline__ uint32_t key_bits(float v) { return __float_as_uint(v
 __device__ __forceinline__ uint32_t key_bits(double v) { return __float_as_uint(__double2float_rd(v)); }
 static constexpr uint32_t KEY_INF = 0x7f800000u;
 
+// Shared-memory access through 32-bit shared-window addresses.  The sweep loops form every
+// address from bases pinned in registers by a volatile conversion (the compiler otherwise
+// rematerialises the window base with S2R on each step under the register cap); the volatile
+// accesses keep program order and are not moved across barriers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    uint32_t a;
+    asm volatile("mov.u32 %0, %1;" : "=r"(a) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return a;
+}
+template <typename T> __device__ __forceinline__ T lds(uint32_t a);
+template <> __device__ __forceinline__ float lds<float>(uint32_t a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ double lds<double>(uint32_t a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(v)); }
+__device__ __forceinline__ void sts(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(v)); }
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" :: "r"(a), "r"(v)); }
+
 // Local solve of Eq. (2) for U at one gridpoint, shifted sorted form (SURVEY
 // C.3, readings R1-R4): a1 <= a2 <= a3 are the per-axis neighbour minima (a1 finite),
 // hf = h/F.  t = U - a1; one-sided t = hf; two-sided iff hf > a2 - a1; three-sided iff the
@@ -442,6 +475,7 @@ template <int R> struct CellShared {
     int32_t lcnt[2], lover;            // active-list lengths / overflow
     uint32_t bwd[2];                   // axes with activations behind the wavefront
     unsigned long long plane0;         // active planes of the first sweep (direction dir0)
+    long long tm[8];                   // phase timers (thread 0 only; diagnostics)
 };
 
 // dynamic shared memory carve-up
@@ -469,13 +503,16 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                                               uint32_t& nupd, uint32_t& nwr, uint32_t& nsteps)
 {
     using C = CellCfg<R>;
-    constexpr int R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
+    constexpr int R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL, NT = C::NT;
+    constexpr int TS = (int)sizeof(T);
     constexpr bool fx = DIR & 1, fy = DIR & 2, fz = DIR & 4;
     const int tid = threadIdx.x;
-    T* sV = M.V;
-    T* sH = M.H;
-    uint8_t* sA = M.act;
     const T INF = dinf<T>();
+    // shared-window bases: V box (at the first interior point), hf, activity bytes
+    const uint32_t vb = smem_u32(M.V) + (uint32_t)((1 + RP + RP2) * TS);
+    const uint32_t hb = smem_u32(M.H);
+    const uint32_t ab = smem_u32(M.act);
+    const uint32_t scratch = ab + R3;   // activity stores that do not apply go here
     bool fwd = false;
     uint32_t bwd = 0;
     int s = __ffsll((long long)pm) - 1;
@@ -483,25 +520,29 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     // a + b + c = s.  The point index is p = e XOR dm (R a power of two: reflecting an axis
     // XORs its field); in canonical coordinates "forward" along an axis is +1 and the
     // forward / backward neighbours exist iff the coordinate is < R-1 / > 0.  Box and flag
-    // offsets of the forward neighbours are per-sweep constants.
+    // offsets (bytes) of the forward neighbours are compile-time constants.
     constexpr unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
-    constexpr int oxq = fx ? -1 : 1, oyq = fy ? -RP : RP, ozq = fz ? -RP2 : RP2;   // box
-    constexpr int oxp = fx ? -1 : 1, oyp = fy ? -R : R, ozp = fz ? -R * R : R * R;  // flags
+    // (unsigned: address arithmetic wraps modulo 2^32, a negative offset subtracts)
+    constexpr uint32_t oxq = (uint32_t)((fx ? -1 : 1) * TS), oyq = (uint32_t)((fy ? -RP : RP) * TS),
+                       ozq = (uint32_t)((fz ? -RP2 : RP2) * TS);
+    constexpr uint32_t oxp = (uint32_t)(fx ? -1 : 1), oyp = (uint32_t)(fy ? -R : R),
+                       ozp = (uint32_t)(fz ? -R * R : R * R);
     // Two-stage prefetch, independent of the current step's results: at step s the thread
     // holds its entry en / hf hn of plane s and the entry en1 of plane s + 1; the step loads
     // hf of plane s + 1 (shared memory) and the entry of plane s + 2 (global table via L1),
     // so no load sits on the step's critical path.  The table has two empty trailing planes.
     const uint16_t* tp = ptab + tid;
-    constexpr int NT = C::NT;
     unsigned en = __ldg(&tp[s * NT]);
     unsigned en1 = __ldg(&tp[(s + 1) * NT]);
-    T hn = en < (unsigned)R3 ? sH[en ^ dm] : INF;
+    T hn = en < (unsigned)R3 ? lds<T>(hb + (en ^ dm) * TS) : INF;
 #define EIK_PREFETCH(sp_)                                                                  \
     {                                                                                  \
         en = en1;                                                                      \
-        hn = en < (unsigned)R3 ? sH[en ^ dm] : INF;                                    \
+        hn = en < (unsigned)R3 ? lds<T>(hb + (en ^ dm) * TS) : INF;                    \
         en1 = __ldg(&tp[((sp_) + 1) * NT]);                                            \
     }
+    // box byte offset of point p = a + R b + R^2 c (relative to vb)
+#define EIK_QOFF(up_) ((((up_) & (R - 1)) + RP * (((up_) / R) & (R - 1)) + RP2 * ((up_) / (R * R))) * TS)
     // First sweep of a cell with many active points (a fresh cell the front is entering):
     // relax every point of every plane without per-point gating -- nearly all of them
     // change anyway -- and record only the activations *behind* the wavefront, which the
@@ -512,29 +553,28 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
             const T hs = hn;
             EIK_PREFETCH(s + 1)
             if (ue < (unsigned)R3) {
-                const int p = (int)(ue ^ dm);
-                EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
-                sA[p] = 0;                                             // Alg. 2 line 4
-                const unsigned up = (unsigned)p;
-                const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
-                const T v = sV[q];
-                const T xf = sV[q + oxq], xb = sV[q - oxq];
-                const T yf = sV[q + oyq], yb = sV[q - oyq];
-                const T zf = sV[q + ozq], zb = sV[q - ozq];
+                const unsigned up = ue ^ dm;
+                EIK_CHECK(up < (unsigned)R3, "wavefront point index");
+                sts_u8(ab + up, 0u);                                   // Alg. 2 line 4
+                const uint32_t qa = vb + EIK_QOFF(up);
+                const T v = lds<T>(qa);
+                const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
+                const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
+                const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
                 const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
                 const T hf = fabs(hs);
                 if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
                     ++nupd;
                     const T u = local_solve_fast<T>(mx, my, mz, hf);
                     if (u < v) {
-                        sV[q] = u;
-                        if (hs > T(0)) sH[p] = -hs;
+                        sts(qa, u);
+                        if (hs > T(0)) sts(hb + up * TS, -hs);
                         ++nwr;
                         const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
                         const int bxa = (xb > u) & (ca > 0), bya = (yb > u) & (cb > 0), bza = (zb > u) & (cc > 0);
-                        sA[bxa ? p - oxp : R3] = 1;
-                        sA[bya ? p - oyp : R3] = 1;
-                        sA[bza ? p - ozp : R3] = 1;
+                        sts_u8(bxa ? ab + up - oxp : scratch, 1u);
+                        sts_u8(bya ? ab + up - oyp : scratch, 1u);
+                        sts_u8(bza ? ab + up - ozp : scratch, 1u);
                         bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
                     }
                 }
@@ -555,25 +595,23 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
         EIK_PREFETCH(s + 1)   // independent of this step's results
         bool myfwd = false;
         if (ue < (unsigned)R3) {
-            const int p = (int)(ue ^ dm);
-            EIK_CHECK(p >= 0 && p < R3, "wavefront point index");
-            if (sA[p]) {
-                sA[p] = 0;                                             // Alg. 2 line 4
-                const unsigned up = (unsigned)p;
-                const int q = (int)((up & (R - 1)) + RP * ((up / R) & (R - 1)) + RP2 * (up / (R * R))) + (1 + RP + RP2);
-                EIK_CHECK(q - RP2 >= 0 && q + RP2 < C::BOX, "box index");
-                const T v = sV[q];
-                const T xf = sV[q + oxq], xb = sV[q - oxq];
-                const T yf = sV[q + oyq], yb = sV[q - oyq];
-                const T zf = sV[q + ozq], zb = sV[q - ozq];
+            const unsigned up = ue ^ dm;
+            EIK_CHECK(up < (unsigned)R3, "wavefront point index");
+            if (lds_u8(ab + up)) {
+                sts_u8(ab + up, 0u);                                   // Alg. 2 line 4
+                const uint32_t qa = vb + EIK_QOFF(up);
+                const T v = lds<T>(qa);
+                const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
+                const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
+                const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
                 const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
                 const T hf = fabs(hs);
                 if (hf < INF && fmin(mx, fmin(my, mz)) < v) {          // fixed / no gain
                     ++nupd;
                     const T u = local_solve_fast<T>(mx, my, mz, hf);    // line 5
                     if (u < v) {                                         // line 6
-                        sV[q] = u;                                       // line 7
-                        if (hs > T(0)) sH[p] = -hs;                      // mark changed
+                        sts(qa, u);                                      // line 7
+                        if (hs > T(0)) sts(hb + up * TS, -hs);           // mark changed
                         ++nwr;
                         // lines 8-13: activate larger in-cell neighbours (the cross-border
                         // "currently downwind" test is done once per processing)
@@ -583,12 +621,12 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                         const int fxa = (xf > u) & (ca < R - 1), bxa = (xb > u) & (ca > 0);
                         const int fya = (yf > u) & (cb < R - 1), bya = (yb > u) & (cb > 0);
                         const int fza = (zf > u) & (cc < R - 1), bza = (zb > u) & (cc > 0);
-                        sA[fxa ? p + oxp : R3] = 1;
-                        sA[bxa ? p - oxp : R3] = 1;
-                        sA[fya ? p + oyp : R3] = 1;
-                        sA[bya ? p - oyp : R3] = 1;
-                        sA[fza ? p + ozp : R3] = 1;
-                        sA[bza ? p - ozp : R3] = 1;
+                        sts_u8(fxa ? ab + up + oxp : scratch, 1u);
+                        sts_u8(bxa ? ab + up - oxp : scratch, 1u);
+                        sts_u8(fya ? ab + up + oyp : scratch, 1u);
+                        sts_u8(bya ? ab + up - oyp : scratch, 1u);
+                        sts_u8(fza ? ab + up + ozp : scratch, 1u);
+                        sts_u8(bza ? ab + up - ozp : scratch, 1u);
                         myfwd = (fxa | fya | fza) != 0;
                         bwd |= (unsigned)(bxa | (bya << 1) | (bza << 2));
                     }
@@ -598,6 +636,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
         fwd = __syncthreads_or(myfwd);
         ++nsteps;
     }
+#undef EIK_QOFF
 #undef EIK_PREFETCH
     return bwd;
 }
@@ -650,7 +689,10 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
     }
-    long long tc0 = clock64(), tmask = 0, tstep = 0, nlist = 0, tsa = 0, tsb = 0;
+    // phase timers live in shared memory, written by thread 0 only (no registers held
+    // across the sweeps): tm = {start, tile staged, halo staged, init done, mask, steps, list
+    // iterations, face summaries start}
+    if (tid == 0) { S.tm[0] = clock64(); S.tm[4] = 0; S.tm[5] = 0; S.tm[6] = 0; }
     uint32_t nsteps = 0;
     constexpr int NWB = R3 / 32;   // saved-bitmask words
 
@@ -690,7 +732,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             }
         }
         __syncthreads();
-        tsa = clock64();
+        if (tid == 0) S.tm[1] = clock64();
         constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
         T hv[PH];
         int hq[PH];
@@ -727,7 +769,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // points saved at a sweep cap.  The first sweep's direction is fixed by the inflow faces,
     // so its set of active planes is collected here (no separate scan) ----
     __syncthreads();
-    tsb = clock64();
+    if (tid == 0) S.tm[2] = clock64();
     const int dir0 = (init || !(flags & 63u)) ? 0 :
         (((flags & 2u) && !(flags & 1u) ? 1 : 0) | ((flags & 8u) && !(flags & 4u) ? 2 : 0) |
          ((flags & 32u) && !(flags & 16u) ? 4 : 0));
@@ -787,7 +829,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         if ((tid & 31) == 0 && cnt) { atomicAdd(&S.nact, cnt); atomicOr(&S.plane0, pm0); }
     }
     __syncthreads();
-    const long long tc1 = clock64();
+    if (tid == 0) S.tm[3] = clock64();
 
     int gi = 0, prev_dir = -1;
     int lf0 = -1, lf1 = -1, lf2 = -1;   // sweep at which each axis was last reversed
@@ -800,7 +842,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         // ================= active-list relaxation (few active points) =================
         if (nact <= LCAP) {
             ran_list = true;
-            const long long tl0 = clock64();
+            const long long tl0 = tid == 0 ? clock64() : 0;
             // build the list from the flags
             if (tid == 0) { S.lcnt[0] = 0; S.lcnt[1] = 0; S.lover = 0; }
             __syncthreads();
@@ -822,7 +864,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             while (!overflow) {
                 const int n = S.lcnt[cur];
                 if (n == 0) break;
-                ++nlist;
+                if (tid == 0) ++S.tm[6];
                 uint16_t* Lc = M.list + cur * LCAP;
                 uint16_t* Ln = M.list + (cur ^ 1) * LCAP;
                 for (int t = tid; t < n; t += NT) {
@@ -877,7 +919,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 cur ^= 1;
                 __syncthreads();
             }
-            tstep += clock64() - tl0;
+            if (tid == 0) S.tm[5] += clock64() - tl0;
             if (!overflow) break;          // converged in list mode
             nact = LCAP + 1;               // resume wavefront sweeps (flags authoritative)
         }
@@ -911,7 +953,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             prev_dir = dir;
         }
         const bool fx = dir & 1, fy = dir & 2, fz = dir & 4;
-        const long long tm0 = clock64();
+        const long long tm0 = tid == 0 ? clock64() : 0;
         // the set of planes (in this direction) holding active points, and their count (the
         // first sweep's was collected with the initial activity)
         const bool first = sw == 0 && !ran_list;
@@ -940,8 +982,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         const unsigned long long pm = first ? S.plane0 : S.plane[sw & 1];
         nact = first ? S.nact : S.nact2[sw & 1];
         if (tid == 0) { S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0; }
-        const long long tm1 = clock64();
-        tmask += tm1 - tm0;
+        const long long tm1 = tid == 0 ? clock64() : 0;
+        if (tid == 0) S.tm[4] += tm1 - tm0;
         if (pm == 0ull) break;
         if (nact <= LCAP && sw > 0) continue;   // few left: list mode (next iteration)
         if (A.max_sweeps > 0 && nsweeps >= (uint32_t)A.max_sweeps) {
@@ -981,13 +1023,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             default: bwd = sweep_dir<T, R, 7>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
             }
         }
-        tstep += clock64() - tm1;
+        if (tid == 0) S.tm[5] += clock64() - tm1;
         nact = LCAP + 1;   // unknown until the next scan
         for (int o = 16; o > 0; o >>= 1) bwd |= __shfl_xor_sync(0xffffffffu, bwd, o);
         if ((tid & 31) == 0 && bwd) atomicOr(&S.bwd[sw & 1], bwd);
         __syncthreads();
     }
-    const long long tc2 = clock64();
+    if (tid == 0) S.tm[7] = clock64();
     // ---- face summaries (Eq. (3)): face f is currently downwind iff a border
     // point changed in this processing and ended below its outside neighbour (the staged
     // halo value, an upper bound of the current one: P:718 redundant tags are harmless); the
@@ -1066,14 +1108,14 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     }
     n_sweeps_out = nsweeps;
     if (tid == 0 && A.stats) {
-        atomicAdd(&A.ctl->dbg[36], (unsigned long long)(tc1 - tc0));
-        atomicAdd(&A.ctl->dbg[41], (unsigned long long)(tsa - tc0));
-        atomicAdd(&A.ctl->dbg[42], (unsigned long long)(tsb - tsa));
-        atomicAdd(&A.ctl->dbg[37], (unsigned long long)tmask);
-        atomicAdd(&A.ctl->dbg[38], (unsigned long long)tstep);
-        atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - tc2));
+        atomicAdd(&A.ctl->dbg[36], (unsigned long long)(S.tm[3] - S.tm[0]));
+        atomicAdd(&A.ctl->dbg[41], (unsigned long long)(S.tm[1] - S.tm[0]));
+        atomicAdd(&A.ctl->dbg[42], (unsigned long long)(S.tm[2] - S.tm[1]));
+        atomicAdd(&A.ctl->dbg[37], (unsigned long long)S.tm[4]);
+        atomicAdd(&A.ctl->dbg[38], (unsigned long long)S.tm[5]);
+        atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - S.tm[7]));
         atomicAdd(&A.ctl->dbg[2], (unsigned long long)nsteps);
-        atomicAdd(&A.ctl->dbg[40], (unsigned long long)nlist);
+        atomicAdd(&A.ctl->dbg[40], (unsigned long long)S.tm[6]);
     }
 }
 

@@ -273,6 +273,7 @@ extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
     for (int i = 42; i < n && i < 42 + 2048; ++i) out[i] = ctx->ctl_host->rtrace[i - 42];
     if (n > 42 + 2048) out[42 + 2048] = ctx->ctl_host->dbg[41];
     if (n > 43 + 2048) out[43 + 2048] = ctx->ctl_host->dbg[42];
+    for (int i = 44 + 2048; i < n && i < 44 + 4096; ++i) out[i] = ctx->ctl_host->rtrace2[i - 44 - 2048];
     return EIK_OK;
 }
 
@@ -419,8 +420,9 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
     }
     // loop mode 2: rounds in a CUDA graph with a conditional WHILE node around one round
     char keybuf[256];
-    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%p/%p/%g/%d", (int)sizeof(T), r, (long long)J,
-             ca.Vt, ca.Ht, ctx->bin_width, ctx->collect_stats);
+    // every value baked into the captured kernel parameters is part of the key
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d", (int)sizeof(T), r, (long long)J,
+             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps);
     if (!ctx->gexec || ctx->gkey != keybuf) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
         cudaGraph_t graph;

@@ -186,6 +186,8 @@ struct Ctl {
     uint32_t q_head, q_tail, pending, abort;   // async mode ring + work counter
     unsigned long long t_solve0, budget_ns;     // watchdog: abort after budget_ns
     uint32_t rtrace[2048];                      // round mode: per-round (cells, span ns)
+    uint32_t rtrace2[2048];                     // round mode: per-round (sum cycles / 1024, max cycles)
+    unsigned long long rsum, rmax;              // this round's processing cycles (stats)
     uint32_t claim;                             // round mode: next cell of this round
     unsigned long long defers;
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
@@ -374,10 +376,14 @@ __device__ __forceinline__ bool round_end_body(Ctl* ctl)
         if (ctl->rounds <= 1024u) {   // per-round trace (diagnostics): cells, span ns
             ctl->rtrace[2 * (ctl->rounds - 1)] = ctl->proc_count;
             ctl->rtrace[2 * (ctl->rounds - 1) + 1] = (uint32_t)(ctl->t_end - ctl->t_start);
+            ctl->rtrace2[2 * (ctl->rounds - 1)] = (uint32_t)(ctl->rsum >> 10);
+            ctl->rtrace2[2 * (ctl->rounds - 1) + 1] = (uint32_t)ctl->rmax;
         }
     }
     ctl->t_start = ~0ull;
     ctl->t_end = 0;
+    ctl->rsum = 0;
+    ctl->rmax = 0;
     ctl->proc_count = 0;
     ctl->claim = 0;
     ctl->wl_count[cur] = 0;
@@ -1213,6 +1219,8 @@ k_cell(CellArgs A)
             atomicAdd(&ctl->dbg[0], cyc);
             atomicMax(&ctl->dbg[1], cyc);
             atomicAdd(&ctl->dbg[3], 1ull);
+            atomicAdd(&ctl->rsum, cyc);
+            atomicMax(&ctl->rmax, cyc);
         }
         __syncthreads();   // smem reuse by the next cell of this CTA
     }

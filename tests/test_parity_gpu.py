@@ -146,6 +146,27 @@ def test_schedule_independence(mode, delta, msw, defer):
     s.close()
 
 
+def test_option_change_between_solves_takes_effect():
+    """The round loop is a cached CUDA graph: an option baked into its kernel parameters (the
+    sweep cap) must invalidate it, and a grid with the same cell count but another n must not
+    reuse stale geometry."""
+    import paper_1306_4743_b200 as eik
+    s = eik.Solver(device=0)
+    w = W.c3(64)
+    s.set_option(eik.EIK_OPT_MAX_SWEEPS, 0)
+    _gpu(s, w, np.float32, 16)
+    uncapped = s.debug()["sweep_hist"]
+    assert any(uncapped[2:]), "C3 should need > 1 sweep somewhere without a cap"
+    s.set_option(eik.EIK_OPT_MAX_SWEEPS, 1)
+    assert_parity(_gpu(s, w, np.float32, 16), oracle_U(w), w, np.float32)
+    assert not any(s.debug()["sweep_hist"][2:]), "sweep cap 1 ignored (stale graph)"
+    for n in (60, 63):   # same cps = 4 at r = 16, different n
+        wn = W.c2(n) if n % 2 == 0 else W.random_instance(n, 7, p_wall=0.1, n_exits=2)
+        assert_parity(_gpu(s, wn, np.float32, 16), oracle_U(wn), wn, np.float32)
+        assert s.stats()["M"] == (n + 1) ** 3
+    s.close()
+
+
 def test_stats_are_consistent(solver):
     w = W.c1(64)
     _gpu(solver, w, np.float64, 8)

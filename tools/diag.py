@@ -18,11 +18,14 @@ for name in cfgs:
         for kv in parts[1:]:
             k, v = kv.split("=")
             if k == "bw": bw = float(v)
+            if k == "bwr": bw = -float(v)   # multiple of r*h, resolved below
             if k == "mode": mode = int(v)
             if k == "defer": defer = int(v)
             if k == "msw": msw = int(v)
     cfg, prec, r = bench.WORKLOADS[name]
     n, F, m, q = bench.make_inputs(cfg, prec, torch.device("cuda", 0))
+    if bw is not None and bw < 0:
+        bw = -bw * r * bench.grid_h(cfg, n)
     s = eik.Solver(bin_width=bw, loop_mode=mode)
     if bw is not None and mode == 0:
         s.set_option(eik.EIK_OPT_BIN_WIDTH, bw)

@@ -274,6 +274,7 @@ extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
     if (n > 42 + 2048) out[42 + 2048] = ctx->ctl_host->dbg[41];
     if (n > 43 + 2048) out[43 + 2048] = ctx->ctl_host->dbg[42];
     for (int i = 44 + 2048; i < n && i < 44 + 4096; ++i) out[i] = ctx->ctl_host->rtrace2[i - 44 - 2048];
+    for (int i = 44 + 4096; i < n && i < 44 + 4096 + 12; ++i) out[i] = (&ctx->ctl_host->lstat[0][0])[i - 44 - 4096];
     return EIK_OK;
 }
 

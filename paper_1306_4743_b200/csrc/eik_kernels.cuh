@@ -188,6 +188,8 @@ struct Ctl {
     uint32_t rtrace[2048];                      // round mode: per-round (cells, span ns)
     uint32_t rtrace2[2048];                     // round mode: per-round (sum cycles / 1024, max cycles)
     unsigned long long rsum, rmax;              // this round's processing cycles (stats)
+    unsigned long long lstat[2][6];             // [all, > 100k cycles]: count, cycles, sweeps,
+                                                // list iterations, plane steps, flags CONT
     uint32_t claim;                             // round mode: next cell of this round
     unsigned long long defers;
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
@@ -482,6 +484,7 @@ template <int R> struct CellShared {
     uint32_t bwd[2];                   // axes with activations behind the wavefront
     unsigned long long plane0;         // active planes of the first sweep (direction dir0)
     long long tm[8];                   // phase timers (thread 0 only; diagnostics)
+    uint32_t nsteps;                   // plane steps of this processing (diagnostics)
 };
 
 // dynamic shared memory carve-up
@@ -1121,6 +1124,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         atomicAdd(&A.ctl->dbg[38], (unsigned long long)S.tm[5]);
         atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - S.tm[7]));
         atomicAdd(&A.ctl->dbg[2], (unsigned long long)nsteps);
+        S.nsteps = nsteps;
         atomicAdd(&A.ctl->dbg[40], (unsigned long long)S.tm[6]);
     }
 }
@@ -1221,6 +1225,15 @@ k_cell(CellArgs A)
             atomicAdd(&ctl->dbg[3], 1ull);
             atomicAdd(&ctl->rsum, cyc);
             atomicMax(&ctl->rmax, cyc);
+            for (int l = 0; l < 2; ++l) {
+                if (l == 1 && cyc <= 100000ull) break;
+                atomicAdd(&ctl->lstat[l][0], 1ull);
+                atomicAdd(&ctl->lstat[l][1], cyc);
+                atomicAdd(&ctl->lstat[l][2], nsw);
+                atomicAdd(&ctl->lstat[l][3], (unsigned long long)S.tm[6]);
+                atomicAdd(&ctl->lstat[l][4], (unsigned long long)S.nsteps);
+                atomicAdd(&ctl->lstat[l][5], (A.proc_flags[w] & FLAG_CONT) ? 1ull : 0ull);
+            }
         }
         __syncthreads();   // smem reuse by the next cell of this CTA
     }

@@ -566,7 +566,12 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
                     (unsigned long long)ctx->ctl_host->processings);
     if (ctx->ctl_host->abort)
         return fail(ctx, EIK_EINTERNAL, "processing limit exceeded (async scheduler)");
-    k_egress<T><<<(int)(n1 * n1 < (int64_t)G * 16 ? n1 * n1 : (int64_t)G * 16), 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
+    {
+        const int64_t nv = ((n1 + 3) / 4) * n1;   // vectors per z-plane
+        const int bx = (int)((nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64);
+        const int by = (int)(n1 < 65535 ? n1 : 65535);
+        k_egress<T><<<dim3(bx, by), 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[3], s));
     CK(cudaEventSynchronize(ctx->ev[3]));

@@ -235,6 +235,18 @@ __device__ __forceinline__ void warp_agg_append(uint32_t* counter, uint32_t* lis
 // --------------------------------------------------------------------------------------
 // A1/A2: ingest + validate + seed
 // --------------------------------------------------------------------------------------
+template <typename T> struct Vec4T;
+template <> struct Vec4T<float> { static __device__ __forceinline__ void st(float* p, const float* v) {
+    __stcg(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3])); } 
+    static __device__ __forceinline__ void ld(const float* p, float* v) {
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(p)); v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w; } };
+template <> struct Vec4T<double> { static __device__ __forceinline__ void st(double* p, const double* v) {
+    __stcg(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    __stcg(reinterpret_cast<double2*>(p) + 1, make_double2(v[2], v[3])); }
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+    const double2 x = __ldcg(reinterpret_cast<const double2*>(p)), y = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; } };
+
 template <typename T>
 __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __restrict__ mask,
                          const T* __restrict__ q, T* __restrict__ Vt, T* __restrict__ Ht,
@@ -245,26 +257,45 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
     const int64_t n1 = g.n1;
     const uint32_t cps = (uint32_t)g.cps;
     uint32_t exits = 0;
-    // shift/mask index math (r a power of two); one 32-bit division pair per point for the
-    // cell coordinates (J < 2^31)
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t c = (uint32_t)(p >> (3 * lr));
-        const int e = (int)(p & ((1 << (3 * lr)) - 1));
-        const int a = e & (r - 1), b = (e >> lr) & (r - 1), d = e >> (2 * lr);
+    // four consecutive points of one tile row per thread (r >= 4, rows 16-byte aligned in the
+    // tiles): vector tile stores and four independent F / mask loads in flight per thread
+    // (the lexicographic rows are not 16-byte aligned: n + 1 is odd in general).  Shift/mask
+    // index math (r a power of two); one 32-bit division pair per vector (J < 2^31).
+    const int64_t P4 = P >> 2;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < P4;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p0 = v << 2;
+        const uint32_t c = (uint32_t)(p0 >> (3 * lr));
+        const int e0 = (int)(p0 & ((1 << (3 * lr)) - 1));
+        const int a0 = e0 & (r - 1), b = (e0 >> lr) & (r - 1), d = e0 >> (2 * lr);
         const uint32_t cxy = c % (cps * cps);
         const int cx = (int)(cxy % cps), cy = (int)(cxy / cps), cz = (int)(c / (cps * cps));
-        const int64_t i = (int64_t)(cx << lr) + a, j = (int64_t)(cy << lr) + b, k = (int64_t)(cz << lr) + d;
-        T v = dinf<T>(), hf = dinf<T>();
-        if (i < n1 && j < n1 && k < n1) {
-            const int64_t lex = i + n1 * (j + n1 * k);
-            const T f = F[lex];
-            if (!(f >= T(0)) || !(f < dinf<T>())) atomicOr(&ctl->err, 1u);   // F < 0, NaN, inf
-            if (mask[lex]) {
-                T qv = q[lex];
+        const int64_t i0 = (int64_t)(cx << lr) + a0, j = (int64_t)(cy << lr) + b, k = (int64_t)(cz << lr) + d;
+        const bool row_in = j < n1 && k < n1;
+        const int64_t lex0 = i0 + n1 * (j + n1 * k);
+        T f[4];
+        uint8_t mk[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const bool in = row_in && i0 + l < n1;
+            f[l] = in ? __ldcs(&F[lex0 + l]) : T(0);
+            mk[l] = in ? __ldcs(&mask[lex0 + l]) : (uint8_t)0;
+        }
+        T vv[4], hh[4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            vv[l] = dinf<T>();
+            hh[l] = dinf<T>();
+            if (!(row_in && i0 + l < n1)) continue;
+            const T fl = f[l];
+            if (!(fl >= T(0)) || !(fl < dinf<T>())) atomicOr(&ctl->err, 1u);   // F < 0, NaN, inf
+            if (mk[l]) {
+                const int a = a0 + l;
+                const int64_t i = i0 + l;
+                T qv = q[lex0 + l];
                 if (!(qv >= T(0)) || !(qv < dinf<T>())) atomicOr(&ctl->err, 2u);
                 qv = qv + T(0);   // canonicalise -0 -> +0 (R9)
-                v = qv;           // exits: fixed, V = q (hf stays +inf: never updated)
+                vv[l] = qv;       // exits: fixed, V = q (hf stays +inf: never updated)
                 ++exits;
                 const uint32_t kb = key_bits(qv);
                 // V^c of a cell in Q^c = min exit value; cells holding a non-exit
@@ -284,12 +315,12 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
                         atomicMin(&key[cc[f2]], kb);
                         atomicOr(&state[cc[f2]], FLAG_INIT);
                     }
-            } else if (f > T(0)) {
-                hf = h / f;       // +inf for subnormal-overflow: treated as impassable
+            } else if (fl > T(0)) {
+                hh[l] = h / fl;   // +inf for subnormal-overflow: treated as impassable
             }
         }
-        Vt[p] = v;
-        Ht[p] = hf;
+        Vec4T<T>::st(&Vt[p0], vv);
+        Vec4T<T>::st(&Ht[p0], hh);
     }
     // exit count (warp-aggregated)
     for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(0xffffffffu, exits, o);
@@ -1394,19 +1425,27 @@ __global__ void k_seed_queue(uint32_t* state, uint32_t* ring, Ctl* ctl, int64_t 
 template <typename T>
 __global__ void k_egress(Geom g, const T* __restrict__ Vt, T* __restrict__ U, int64_t M)
 {
-    // one (j, k) row of the output per block iteration: coalesced writes along i, tile reads
-    // in runs of r
+    // four consecutive output points of one (j, k) row per thread, flat over the z-plane
+    // (blockIdx.y strides over k): one 16-byte tile read, four coalesced scalar writes
     const int r = g.r, lr = g.lr;
     const int64_t n1 = g.n1;
-    const int64_t cps = g.cps;
-    const int64_t rows = n1 * n1;
-    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-        const int64_t k = row / n1, j = row - k * n1;
-        const int64_t cjk = cps * ((j >> lr) + cps * (k >> lr));
-        const int ejk = r * ((int)(j & (r - 1)) + r * (int)(k & (r - 1)));
-        for (int64_t i = threadIdx.x; i < n1; i += blockDim.x) {
-            const int64_t c = (i >> lr) + cjk;
-            U[row * n1 + i] = Vt[(c << (3 * lr)) + ejk + (int)(i & (r - 1))];
+    const uint32_t cps = (uint32_t)g.cps;
+    const uint32_t n1v = (uint32_t)((n1 + 3) >> 2);      // vectors per row
+    const uint32_t nv = n1v * (uint32_t)n1;              // vectors per z-plane (< 2^32)
+    for (int64_t k = blockIdx.y; k < n1; k += gridDim.y) {
+        const uint32_t ck = (uint32_t)(k >> lr) * cps;
+        const int ek = r * r * (int)(k & (r - 1));
+        for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nv; t += gridDim.x * blockDim.x) {
+            const uint32_t j = t / n1v, iv = t - j * n1v;
+            const int64_t i0 = (int64_t)iv << 2;
+            const uint32_t c = (uint32_t)(i0 >> lr) + cps * ((j >> lr) + ck);
+            const int e = (int)(i0 & (r - 1)) + r * (int)(j & (r - 1)) + ek;
+            T v[4];
+            Vec4T<T>::ld(&Vt[((int64_t)c << (3 * lr)) + e], v);
+            T* out = U + (int64_t)j * n1 + n1 * n1 * k + i0;
+#pragma unroll
+            for (int l = 0; l < 4; ++l)
+                if (i0 + l < n1) __stcs(&out[l], v[l]);
         }
     }
 }

@@ -492,8 +492,13 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     const int G = ctx->sm_count * 8;
     k_init_cells<<<G, 256, 0, s>>>(ctx->key, ctx->state, J, ctx->ctl);
     Geom g{n1, cps, r, r == 4 ? 2 : r == 8 ? 3 : 4};
-    k_ingest<T><<<G * 2, 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt, (T*)ctx->Ht,
-                                      ctx->key, ctx->state, ctx->ctl, P);
+    {
+        const int64_t np = (int64_t)cps * r, nv = (np / 4) * np;   // vectors per padded z-plane
+        const int bx = (int)((nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64);
+        const int by = (int)(np < 65535 ? np : 65535);
+        k_ingest<T><<<dim3(bx, by), 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt,
+                                                 (T*)ctx->Ht, ctx->key, ctx->state, ctx->ctl, P);
+    }
     if (ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
     // input validation result (device-detected errors return before touching U_out)

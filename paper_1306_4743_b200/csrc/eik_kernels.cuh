@@ -257,71 +257,90 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
     const int64_t n1 = g.n1;
     const uint32_t cps = (uint32_t)g.cps;
     uint32_t exits = 0;
-    // four consecutive points of one tile row per thread (r >= 4, rows 16-byte aligned in the
-    // tiles): vector tile stores and four independent F / mask loads in flight per thread
-    // (the lexicographic rows are not 16-byte aligned: n + 1 is odd in general).  Shift/mask
-    // index math (r a power of two); one 32-bit division pair per vector (J < 2^31).
-    const int64_t P4 = P >> 2;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < P4;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p0 = v << 2;
-        const uint32_t c = (uint32_t)(p0 >> (3 * lr));
-        const int e0 = (int)(p0 & ((1 << (3 * lr)) - 1));
-        const int a0 = e0 & (r - 1), b = (e0 >> lr) & (r - 1), d = e0 >> (2 * lr);
-        const uint32_t cxy = c % (cps * cps);
-        const int cx = (int)(cxy % cps), cy = (int)(cxy / cps), cz = (int)(c / (cps * cps));
-        const int64_t i0 = (int64_t)(cx << lr) + a0, j = (int64_t)(cy << lr) + b, k = (int64_t)(cz << lr) + d;
-        const bool row_in = j < n1 && k < n1;
-        const int64_t lex0 = i0 + n1 * (j + n1 * k);
-        T f[4];
-        uint8_t mk[4];
+    // Lexicographic traversal of the padded grid (cps r)^3, four consecutive i per thread:
+    // a warp reads 512 contiguous bytes of F (the rows are not 16-byte aligned, so four scalar
+    // loads) and writes 16-byte aligned pieces of eight tile rows.  (A tile-order traversal
+    // reads 64-byte row pieces at unaligned offsets and over-fetches F 2x, the mask 4x.)
+    // blockIdx.y strides over k; 32-bit index math within a z-plane.
+    const uint32_t np = cps << lr;             // padded points per side
+    const uint32_t nvr = np >> 2;              // vectors per padded row
+    const uint32_t nv = nvr * np;              // vectors per padded z-plane (< 2^32)
+    // two vectors per thread and iteration (t and t + S): eight loads of F and eight of the
+    // mask in flight before any is used
+    const uint32_t S = gridDim.x * blockDim.x;
+    for (int64_t k = blockIdx.y; k < (int64_t)np; k += gridDim.y)
+    for (uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < nv; t0 += 2 * S) {
+        T f[2][4];
+        uint8_t mk[2][4];
+        int64_t i0[2], j[2], lex0[2], p0[2];
+        uint32_t c[2];
+        bool vin[2], row_in[2];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            const bool in = row_in && i0 + l < n1;
-            f[l] = in ? __ldcs(&F[lex0 + l]) : T(0);
-            mk[l] = in ? __ldcs(&mask[lex0 + l]) : (uint8_t)0;
-        }
-        T vv[4], hh[4];
+        for (int u = 0; u < 2; ++u) {
+            const uint32_t t = t0 + u * S;
+            vin[u] = t < nv;
+            const uint32_t j32 = t / nvr, iv = t - j32 * nvr;
+            i0[u] = (int64_t)iv << 2;
+            j[u] = j32;
+            const int a0 = (int)(i0[u] & (r - 1)), b = (int)(j[u] & (r - 1)), d = (int)(k & (r - 1));
+            c[u] = (uint32_t)(i0[u] >> lr) + cps * ((uint32_t)(j[u] >> lr) + cps * (uint32_t)(k >> lr));
+            p0[u] = ((int64_t)c[u] << (3 * lr)) + a0 + r * (b + r * d);
+            row_in[u] = vin[u] && j[u] < n1 && k < n1;
+            lex0[u] = i0[u] + n1 * (j[u] + n1 * k);
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            vv[l] = dinf<T>();
-            hh[l] = dinf<T>();
-            if (!(row_in && i0 + l < n1)) continue;
-            const T fl = f[l];
-            if (!(fl >= T(0)) || !(fl < dinf<T>())) atomicOr(&ctl->err, 1u);   // F < 0, NaN, inf
-            if (mk[l]) {
-                const int a = a0 + l;
-                const int64_t i = i0 + l;
-                T qv = q[lex0 + l];
-                if (!(qv >= T(0)) || !(qv < dinf<T>())) atomicOr(&ctl->err, 2u);
-                qv = qv + T(0);   // canonicalise -0 -> +0 (R9)
-                vv[l] = qv;       // exits: fixed, V = q (hf stays +inf: never updated)
-                ++exits;
-                const uint32_t kb = key_bits(qv);
-                // V^c of a cell in Q^c = min exit value; cells holding a non-exit
-                // neighbour of an exit across a cell face are seeded too (R18)
-                atomicMin(&key[c], kb);
-                atomicOr(&state[c], FLAG_INIT);
-                const int64_t c64 = (int64_t)c, cp = (int64_t)cps;
-                const int64_t cc[6] = {a == 0 && i > 0 ? c64 - 1 : -1,
-                                       a == r - 1 && i + 1 < n1 ? c64 + 1 : -1,
-                                       b == 0 && j > 0 ? c64 - cp : -1,
-                                       b == r - 1 && j + 1 < n1 ? c64 + cp : -1,
-                                       d == 0 && k > 0 ? c64 - cp * cp : -1,
-                                       d == r - 1 && k + 1 < n1 ? c64 + cp * cp : -1};
-#pragma unroll
-                for (int f2 = 0; f2 < 6; ++f2)
-                    if (cc[f2] >= 0) {
-                        atomicMin(&key[cc[f2]], kb);
-                        atomicOr(&state[cc[f2]], FLAG_INIT);
-                    }
-            } else if (fl > T(0)) {
-                hh[l] = h / fl;   // +inf for subnormal-overflow: treated as impassable
+            for (int l = 0; l < 4; ++l) {
+                const bool in = row_in[u] && i0[u] + l < n1;
+                f[u][l] = in ? __ldcs(&F[lex0[u] + l]) : T(0);
+                mk[u][l] = in ? __ldcs(&mask[lex0[u] + l]) : (uint8_t)0;
             }
         }
-        Vec4T<T>::st(&Vt[p0], vv);
-        Vec4T<T>::st(&Ht[p0], hh);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (!vin[u]) continue;
+            const int a0 = (int)(i0[u] & (r - 1)), b = (int)(j[u] & (r - 1)), d = (int)(k & (r - 1));
+            T vv[4], hh[4];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                vv[l] = dinf<T>();
+                hh[l] = dinf<T>();
+                if (!(row_in[u] && i0[u] + l < n1)) continue;
+                const T fl = f[u][l];
+                if (!(fl >= T(0)) || !(fl < dinf<T>())) atomicOr(&ctl->err, 1u);   // F < 0, NaN, inf
+                if (mk[u][l]) {
+                    const int a = a0 + l;
+                    const int64_t i = i0[u] + l, jj = j[u];
+                    T qv = q[lex0[u] + l];
+                    if (!(qv >= T(0)) || !(qv < dinf<T>())) atomicOr(&ctl->err, 2u);
+                    qv = qv + T(0);   // canonicalise -0 -> +0 (R9)
+                    vv[l] = qv;       // exits: fixed, V = q (hf stays +inf: never updated)
+                    ++exits;
+                    const uint32_t kb = key_bits(qv);
+                    // V^c of a cell in Q^c = min exit value; cells holding a
+                    // non-exit neighbour of an exit across a cell face are seeded too (R18)
+                    atomicMin(&key[c[u]], kb);
+                    atomicOr(&state[c[u]], FLAG_INIT);
+                    const int64_t c64 = (int64_t)c[u], cp = (int64_t)cps;
+                    const int64_t cc[6] = {a == 0 && i > 0 ? c64 - 1 : -1,
+                                           a == r - 1 && i + 1 < n1 ? c64 + 1 : -1,
+                                           b == 0 && jj > 0 ? c64 - cp : -1,
+                                           b == r - 1 && jj + 1 < n1 ? c64 + cp : -1,
+                                           d == 0 && k > 0 ? c64 - cp * cp : -1,
+                                           d == r - 1 && k + 1 < n1 ? c64 + cp * cp : -1};
+#pragma unroll
+                    for (int f2 = 0; f2 < 6; ++f2)
+                        if (cc[f2] >= 0) {
+                            atomicMin(&key[cc[f2]], kb);
+                            atomicOr(&state[cc[f2]], FLAG_INIT);
+                        }
+                } else if (fl > T(0)) {
+                    hh[l] = h / fl;   // +inf for subnormal-overflow: treated as impassable
+                }
+            }
+            Vec4T<T>::st(&Vt[p0[u]], vv);
+            Vec4T<T>::st(&Ht[p0[u]], hh);
+        }
     }
+    (void)P;
     // exit count (warp-aggregated)
     for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(0xffffffffu, exits, o);
     if ((threadIdx.x & 31) == 0 && exits) atomicAdd(&ctl->n_exits, exits);

@@ -336,10 +336,12 @@ template <typename T>
 static int enqueue_round(eik_ctx* ctx, int r, const CellArgs& ca, int sel_grid, int cgrid,
                          bool time_events = false)
 {
-    k_select<<<sel_grid, 256, 0, ctx->stream>>>(ctx->ctl, ctx->wl0, ctx->wl1, ctx->proc_cell,
-                                                 ctx->proc_flags, ctx->key, ctx->state,
-                                                 (float)ctx->bin_width);
-    CK(cudaGetLastError());
+    if (!ca.fused) {   // fused: k_cell selects the whole worklist itself
+        k_select<<<sel_grid, 256, 0, ctx->stream>>>(ctx->ctl, ctx->wl0, ctx->wl1, ctx->proc_cell,
+                                                     ctx->proc_flags, ctx->key, ctx->state,
+                                                     (float)ctx->bin_width);
+        CK(cudaGetLastError());
+    }
     if (time_events) CK(cudaEventRecord(ctx->cev[0], ctx->stream));
     int st;
     if (r == 16) st = launch_cell<T, 16>(ctx, ca, cgrid);
@@ -408,8 +410,10 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
             const bool te = ctx->time_cell_events != 0;
             st = enqueue_round<T>(ctx, r, ca, sg, (int)(n < (uint32_t)cgrid ? n : (uint32_t)cgrid), te);
             if (st) return st;
-            k_round_end<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
-            CK(cudaGetLastError());
+            if (!ca.fused) {   // fused: the last CTA of k_cell ended the round
+                k_round_end<<<1, 1, 0, ctx->stream>>>(ctx->ctl);
+                CK(cudaGetLastError());
+            }
             if (te) {
                 CK(cudaEventSynchronize(ctx->cev[1]));
                 float ms = 0;
@@ -422,8 +426,8 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
     // loop mode 2: rounds in a CUDA graph with a conditional WHILE node around one round
     char keybuf[256];
     // every value baked into the captured kernel parameters is part of the key
-    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d", (int)sizeof(T), r, (long long)J,
-             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps);
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d/%d", (int)sizeof(T), r, (long long)J,
+             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps, ca.fused);
     if (!ctx->gexec || ctx->gkey != keybuf) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
         cudaGraph_t graph;
@@ -445,8 +449,16 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
         ctx->stream = cs;
         CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         const int sg = (int)((J + 255) / 256 < (int64_t)ctx->sm_count * 4 ? (J + 255) / 256 : (int64_t)ctx->sm_count * 4);
-        st = enqueue_round<T>(ctx, r, ca, sg, cgrid);
-        k_round_end_graph<<<1, 1, 0, cs>>>(ctx->ctl, handle);
+        if (ca.fused) {
+            // one kernel per round: k_cell selects, processes and (last CTA) ends the round
+            CellArgs cg = ca;
+            cg.graph = 1;
+            cg.cond = (unsigned long long)handle;
+            st = enqueue_round<T>(ctx, r, cg, sg, cgrid);
+        } else {
+            st = enqueue_round<T>(ctx, r, ca, sg, cgrid);
+            k_round_end_graph<<<1, 1, 0, cs>>>(ctx->ctl, handle);
+        }
         cudaGraph_t captured;
         cudaError_t ce = cudaStreamEndCapture(cs, &captured);
         ctx->stream = saved;
@@ -529,6 +541,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.n1 = n1;
     ca.cps = cps;
     ca.stats = ctx->collect_stats;
+    ca.fused = isinf(ctx->bin_width) ? 1 : 0;
     st = run_loop<T>(ctx, r, J, ca);
     if (st) return st;
     CK(cudaEventRecord(ctx->ev[2], s));

@@ -191,6 +191,7 @@ struct Ctl {
     unsigned long long lstat[2][6];             // [all, > 100k cycles]: count, cycles, sweeps,
                                                 // list iterations, plane steps, flags CONT
     uint32_t claim;                             // round mode: next cell of this round
+    uint32_t cta_done;                          // round mode (fused): CTAs finished this round
     unsigned long long defers;
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
     // steps executed, [3] processings, [4..35] histogram of sweeps per processing (31 = >=31)
@@ -416,8 +417,11 @@ __global__ void k_select(Ctl* ctl, uint32_t* wl0, uint32_t* wl1, uint32_t* proc_
 // --------------------------------------------------------------------------------------
 // round end: swap worklists, count, termination
 // --------------------------------------------------------------------------------------
-__device__ __forceinline__ bool round_end_body(Ctl* ctl)
+// (volatile: in the fused loop this runs in the last CTA of k_cell, whose L1 may hold stale
+// lines of the control block that other CTAs updated with atomics in L2)
+__device__ __forceinline__ bool round_end_body(Ctl* ctl_)
 {
+    volatile Ctl* ctl = ctl_;
     const uint32_t cur = ctl->cur, nx = cur ^ 1u;
     ctl->rounds += 1;
     if (ctl->proc_count > ctl->max_proc) ctl->max_proc = ctl->proc_count;
@@ -438,6 +442,7 @@ __device__ __forceinline__ bool round_end_body(Ctl* ctl)
     ctl->rmax = 0;
     ctl->proc_count = 0;
     ctl->claim = 0;
+    ctl->cta_done = 0;
     ctl->wl_count[cur] = 0;
     ctl->kmin[cur] = KEY_INF;
     ctl->cur = nx;
@@ -499,6 +504,11 @@ struct CellArgs {
     int32_t max_sweeps;              // sweeps per processing before continuing later (0: none)
     uint32_t cap;                    // number of cells J (bounds checks)
     uint32_t* pend;                  // J x R^3/32 saved active bits (FLAG_CONT)
+    int32_t fused;                   // round mode, bin width +inf: k_cell takes its cells straight
+                                     // from the current worklist (the whole list is selected) and
+                                     // its last CTA ends the round (no k_select / k_round_end)
+    int32_t graph;                   // fused + CUDA graph: the last CTA sets the WHILE condition
+    unsigned long long cond;         // cudaGraphConditionalHandle of that WHILE node
 };
 
 // preferred sweep directions from the inflow faces (reading R20): a direction
@@ -1225,24 +1235,46 @@ k_cell(CellArgs A)
     __shared__ CellShared<R> S;
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
-    const uint32_t nproc = ctl->proc_count;
-    const uint32_t nx = ctl->cur ^ 1u;
+    const uint32_t cur = ctl->cur, nx = cur ^ 1u;
+    // fused: this round's cells are the whole current worklist (Alg. 1 lines 4-5 with an
+    // infinite bin); otherwise k_select built the proc list
+    const uint32_t nproc = A.fused ? ctl->wl_count[cur] : ctl->proc_count;
+    const uint32_t* wl = cur ? A.wl1 : A.wl0;
     uint32_t* wn = nx ? A.wl1 : A.wl0;
     // dynamic claiming of this round's cells (processing times vary by >10x between cells)
     bool worked = false;
     for (;;) {
-        if (tid == 0) S.cell = atomicAdd(&ctl->claim, 1u);
+        if (tid == 0) {
+            const uint32_t w = atomicAdd(&ctl->claim, 1u);
+            uint32_t cc = 0xffffffffu, fl = 0;
+            if (w < nproc) {
+                if (A.fused) {
+                    // LIFO: the cells appended last (re-activated by the previous round's
+                    // slowest processings: the critical path) are claimed first
+                    const uint32_t wi = nproc - 1u - w;
+                    cc = wl[wi];
+                    fl = atomicExch(&A.state[cc], 0u);   // take the inflow bits; leaves the list
+                    A.key[cc] = KEY_INF;                 // V^c <- +inf on removal
+                    atomicAdd(&ctl->proc_count, 1u);
+                } else {
+                    cc = A.proc_cell[w];
+                    fl = A.proc_flags[w];
+                }
+            }
+            S.cell = cc;
+            S.flags = fl;
+        }
         __syncthreads();
-        const uint32_t w = S.cell;
-        if (w >= nproc) break;
+        const uint32_t c = S.cell;
+        if (c == 0xffffffffu) break;
         if (!worked && tid == 0) atomicMin(&ctl->t_start, gtimer());
         worked = true;
         const long long t0 = clock64();
-        const uint32_t c = A.proc_cell[w];
         EIK_CHECK(c < A.cap, "round cell id");
+        const uint32_t flags = S.flags;
         if (tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
         unsigned long long nsw = 0;
-        cell_process<T, R>(A, S, Msm, c, A.proc_flags[w], nsw);
+        cell_process<T, R>(A, S, Msm, c, flags, nsw);
         __syncthreads();
         // re-activate currently-downwind neighbour cells (Alg. 1 lines 7-10)
         if (tid < 6 && (S.face_flag & (1u << tid))) {
@@ -1282,12 +1314,22 @@ k_cell(CellArgs A)
                 atomicAdd(&ctl->lstat[l][2], nsw);
                 atomicAdd(&ctl->lstat[l][3], (unsigned long long)S.tm[6]);
                 atomicAdd(&ctl->lstat[l][4], (unsigned long long)S.nsteps);
-                atomicAdd(&ctl->lstat[l][5], (A.proc_flags[w] & FLAG_CONT) ? 1ull : 0ull);
+                atomicAdd(&ctl->lstat[l][5], (flags & FLAG_CONT) ? 1ull : 0ull);
             }
         }
         __syncthreads();   // smem reuse by the next cell of this CTA
     }
     if (worked && tid == 0) atomicMax(&ctl->t_end, gtimer());
+    // fused round end: the last CTA to finish swaps the worklists and decides whether the
+    // loop continues (Alg. 3 line 6); every CTA's appends are ordered before its count
+    if (A.fused && tid == 0) {
+        __threadfence();
+        if (atomicAdd(&ctl->cta_done, 1u) == gridDim.x - 1u) {
+            __threadfence();
+            const bool stop = round_end_body(ctl);
+            if (A.graph) cudaGraphSetConditional((cudaGraphConditionalHandle)A.cond, stop ? 0u : 1u);
+        }
+    }
 }
 
 // ---- async mode: persistent CTAs pull cells from a device FIFO (pHCM Alg. 3 analogue) ---

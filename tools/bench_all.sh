@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+for c in C3 C1 C2 C2d C3d C4 C5 P1 P2 P3 PCB11 PMAZE; do
+  timeout 600 python bench.py --config $c > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
+done
+timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+tail -c 400 gpurun_out/bench_C3.json

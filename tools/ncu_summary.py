@@ -22,7 +22,14 @@ def val(d):
     v = float(d["Metric Value"].replace(",", ""))
     return SCALE.get(d.get("Metric Unit", ""), 1.0) * v
 
-# 1. launch list: share of each kernel in the device time (cold-cache, serialised)
+# 1. launch list: share of each kernel in the device time of ONE solve (cold-cache,
+# serialised).  The profiled command runs several solves (bench warm-up steps); the graph
+# kernels of the round loop may be profiled for only some of them, so every kernel is
+# normalised to one solve: per-round kernels (k_cell, k_select, k_round_end) by the rounds of
+# a solve, once-per-solve kernels by their launch count.
+stats = json.load(open(statsf))["stats"]
+rounds = stats["rounds"]
+PER_ROUND = ("k_cell", "k_select", "k_round_end")
 agg = collections.defaultdict(lambda: [0, 0.0])
 for d in rows_of(launches):
     if d["Metric Name"] != "gpu__time_duration.sum":
@@ -30,19 +37,29 @@ for d in rows_of(launches):
     k = d["Kernel Name"].split("(")[0].replace("void ", "")
     agg[k][0] += 1
     agg[k][1] += val(d)
-tot = sum(v[1] for v in agg.values())
-out["launch_list"] = [{"kernel": k, "launches": c, "us": round(t, 1), "share": round(t / tot, 4)}
-                      for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])]
+per_solve = {}
+for k, (c, t) in agg.items():
+    n_solve = rounds if k.startswith(PER_ROUND) else 1
+    per_solve[k] = (t / c) * n_solve
+tot = sum(per_solve.values())
+out["launch_list"] = [{"kernel": k, "launches_profiled": agg[k][0], "us_per_launch": round(agg[k][1] / agg[k][0], 2),
+                       "us_per_solve": round(t, 1), "share_of_solve": round(t / tot, 4)}
+                      for k, t in sorted(per_solve.items(), key=lambda x: -x[1])]
 
-# 2. k_cell DRAM traffic over all its launches of the profiled solve
-byts = collections.defaultdict(float)
+# 2. k_cell DRAM traffic of the measured solve (the last `rounds` k_cell launches; the
+# profiled command runs a warm-up solve first)
+ids = collections.defaultdict(dict)
 for d in rows_of(kmet):
-    byts[d["Metric Name"]] += val(d)
-stats = json.load(open(statsf))["stats"]
+    ids[int(d["ID"])][d["Metric Name"]] = val(d)
+last = sorted(ids)[-rounds:]
+byts = collections.defaultdict(float)
+for i in last:
+    for m, v in ids[i].items():
+        byts[m] += v
 proc = stats["cell_processings"]
 dram = byts.get("dram__bytes_read.sum", 0) + byts.get("dram__bytes_write.sum", 0)
 out["kcell_traffic"] = {"dram_read": byts.get("dram__bytes_read.sum"), "dram_write": byts.get("dram__bytes_write.sum"),
-                        "time_us": byts.get("gpu__time_duration.sum"), "processings": proc,
+                        "time_us": byts.get("gpu__time_duration.sum"), "launches": len(last), "processings": proc,
                         "dram_bytes_per_processing": dram / max(proc, 1),
                         "alg_bytes_per_processing": stats["bytes_cell_alg"] / max(proc, 1)}
 

@@ -87,6 +87,23 @@ __device__ __forceinline__ void sts(uint32_t a, float v) { asm volatile("st.shar
 __device__ __forceinline__ void sts(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" :: "r"(a), "d"(v)); }
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" :: "r"(a), "r"(v)); }
 
+__device__ __forceinline__ void cp_async_el(uint32_t dst, const float* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_el(uint32_t dst, const double* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
 // Local solve of Eq. (2) for U at one gridpoint, shifted sorted form (SURVEY
 // C.3, readings R1-R4): a1 <= a2 <= a3 are the per-axis neighbour minima (a1 finite),
 // hf = h/F.  t = U - a1; one-sided t = hf; two-sided iff hf > a2 - a1; three-sided iff the
@@ -733,7 +750,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
 // "Changed" is the sign bit of a point's hf; the currently-downwind faces (Eq. (3)) are
 // derived once per processing from the changed border points.  Tile traffic bypasses L1
 // (ld/st .cg): other CTAs update neighbouring tiles concurrently in the async scheduler.
-template <typename T, int R>
+template <typename T, int R, bool CPASYNC>
 __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S,
                                              CellSmem<T, R>& M, uint32_t c, uint32_t flags,
                                              unsigned long long& n_sweeps_out)
@@ -768,7 +785,53 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // ---- stage V and hf with 16-byte vector loads (all of a batch in flight before any
     // store: memory-level parallelism), then the halo N(c) ----
     const bool init = flags & FLAG_INIT;
-    {
+    if constexpr (CPASYNC) {
+        // Round mode: the tile and its hf go out as cp.async (no registers), the halo as
+        // L2 loads issued right behind them -- one memory round trip for all of it.  The
+        // tile's element-wise copies (into the padded box) use .ca, which is safe for the
+        // cell's own tile: no other CTA writes it within a round, and L1 does not survive the
+        // kernel boundary.  The halo must come from L2 (.cg): a neighbour processed earlier in
+        // this round on another SM may have changed it after this SM cached the lines, and its
+        // re-activation of this cell is consumed by this very processing (fused rounds).
+        const uint32_t vs = smem_u32(sV), hs = smem_u32(sH);
+        constexpr int EL = 16 / sizeof(T);
+        for (int vi = tid; vi < R3 / EL; vi += NT) cp_async16(hs + vi * 16, Ht + base + vi * EL);
+        for (int e = tid; e < R3; e += NT) {
+            const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+            cp_async_el(vs + ((a + 1) + RP * (b + 1) + RP2 * (d + 1)) * (int)sizeof(T), Vt + base + e);
+        }
+        constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
+        T hv[PH];
+        int hq[PH];
+#pragma unroll
+        for (int m = 0; m < PH; ++m) {
+            const int e = tid + m * NT;
+            hq[m] = -1;
+            hv[m] = INF;
+            if (e < 6 * R * R) {
+                const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
+                int hx, hy, hz, sa, sb, sd;
+                int64_t nc;
+                bool ex;
+                switch (f) {
+                case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
+                case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
+                case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
+                case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
+                case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
+                default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
+                }
+                hq[m] = (hx + 1) + RP * (hy + 1) + RP2 * (hz + 1);
+                EIK_CHECK(!ex || (nc >= 0 && nc < (int64_t)A.cap), "halo neighbour cell");
+                if (ex) hv[m] = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < PH; ++m)
+            if (hq[m] >= 0) sV[hq[m]] = hv[m];
+        cp_async_wait_all();
+        if (tid == 0) S.tm[1] = clock64();
+    } else {
         using V4 = typename Vec16<T>::type;
         constexpr int EL = 16 / sizeof(T);                // elements per vector
         constexpr int NV = R3 / EL;                       // vectors per tile
@@ -1274,7 +1337,7 @@ k_cell(CellArgs A)
         const uint32_t flags = S.flags;
         if (tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
         unsigned long long nsw = 0;
-        cell_process<T, R>(A, S, Msm, c, flags, nsw);
+        cell_process<T, R, true>(A, S, Msm, c, flags, nsw);
         __syncthreads();
         // re-activate currently-downwind neighbour cells (Alg. 1 lines 7-10)
         if (tid < 6 && (S.face_flag & (1u << tid))) {
@@ -1430,7 +1493,7 @@ k_async(CellArgs A)
         if (c == Q_EMPTY) break;
         const long long t0 = clock64();
         unsigned long long nsw = 0;
-        cell_process<T, R>(A, S, Msm, c, S.flags, nsw);
+        cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
         __threadfence();   // value stores before the re-activations
         __syncthreads();
         if (tid < 6 && (S.face_flag & (1u << tid))) {

@@ -13,8 +13,9 @@ import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # EIK_CHECKS=1 selects the build with device-side bounds checks (libeik_checks.so)
-LIB_PATH = os.path.join(_PKG, "libeik_checks.so" if os.environ.get("EIK_CHECKS") == "1"
-                        else "libeik.so")
+# (EIK_LIB=<path>: an experimental build of the same sources, for tools/ab.py A/B timing)
+LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(
+    _PKG, "libeik_checks.so" if os.environ.get("EIK_CHECKS") == "1" else "libeik.so")
 
 EIK_OK, EIK_EINVAL, EIK_ENOMEM, EIK_ECUDA, EIK_ENOTSUP, EIK_EINTERNAL = range(6)
 EIK_F32, EIK_F64 = 0, 1

@@ -48,6 +48,7 @@ struct eik_ctx {
     uint32_t* proc_cell = nullptr;
     uint32_t* proc_flags = nullptr;
     uint32_t* pend = nullptr;
+    uint32_t* pdir = nullptr;
     uint32_t* gen = nullptr;
     size_t cell_cap = 0;
     size_t ring_cap = 0;
@@ -155,6 +156,11 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     }
     // opt in to > 48 KB dynamic shared memory for the cell kernels
     CK(cudaFuncSetAttribute(k_cell<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
+    // largest shared-memory carveout: the cell kernels are occupancy-limited by shared memory
+    CK(cudaFuncSetAttribute(k_cell<float, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaFuncSetAttribute(k_cell<double, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaFuncSetAttribute(k_async<float, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaFuncSetAttribute(k_async<double, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CK(cudaFuncSetAttribute(k_cell<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 16>()));
     CK(cudaFuncSetAttribute(k_cell<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 8>()));
     CK(cudaFuncSetAttribute(k_cell<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 8>()));
@@ -174,8 +180,9 @@ static void free_scratch(eik_ctx* ctx)
 {
     cudaFree(ctx->Vt); cudaFree(ctx->Ht);
     cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
-    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen);
+    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen); cudaFree(ctx->pdir);
     ctx->pend = nullptr;
+    ctx->pdir = nullptr;
     ctx->gen = nullptr;
     ctx->Vt = ctx->Ht = nullptr;
     ctx->key = ctx->state = ctx->wl0 = ctx->wl1 = ctx->proc_cell = ctx->proc_flags = nullptr;
@@ -303,6 +310,7 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
         CK(cudaMalloc(&ctx->proc_cell, J * 4));
         CK(cudaMalloc(&ctx->proc_flags, J * 4));
         CK(cudaMalloc(&ctx->pend, J * 512));   // R^3 / 8 bytes per cell at r = 16
+        CK(cudaMalloc(&ctx->pdir, J * 4));     // sweep-direction state at a cap
         CK(cudaMalloc(&ctx->gen, J * 4));
         ctx->cell_cap = J;
     }
@@ -537,6 +545,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.max_sweeps = ctx->max_sweeps;
     ca.cap = (uint32_t)J;
     ca.pend = ctx->pend;
+    ca.pdir = ctx->pdir;
     ca.gen = ctx->gen;
     ca.n1 = n1;
     ca.cps = cps;

@@ -488,7 +488,11 @@ template <int R> struct CellCfg {
     static constexpr int LCAP = R == 16 ? 384 : (R == 8 ? 128 : 64);  // active-list capacity
 };
 
+#ifndef EIK_MINB16
+#define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
+#endif
 template <typename T, int R> struct MinBlocks { static constexpr int value = CellCfg<R>::MINB; };
+template <> struct MinBlocks<float, 16> { static constexpr int value = EIK_MINB16; };
 template <> struct MinBlocks<double, 16> { static constexpr int value = 2; };
 
 template <typename T, int R>
@@ -521,6 +525,7 @@ struct CellArgs {
     int32_t max_sweeps;              // sweeps per processing before continuing later (0: none)
     uint32_t cap;                    // number of cells J (bounds checks)
     uint32_t* pend;                  // J x R^3/32 saved active bits (FLAG_CONT)
+    uint32_t* pdir;                  // J: sweep-direction state saved at a sweep cap (FLAG_CONT)
     int32_t fused;                   // round mode, bin width +inf: k_cell takes its cells straight
                                      // from the current worklist (the whole list is selected) and
                                      // its last CTA ends the round (no k_select / k_round_end)
@@ -562,6 +567,7 @@ template <int R> struct CellShared {
     unsigned long long plane0;         // active planes of the first sweep (direction dir0)
     long long tm[8];                   // phase timers (thread 0 only; diagnostics)
     uint32_t nsteps;                   // plane steps of this processing (diagnostics)
+    uint32_t dstate;                   // direction state saved at a sweep cap (pdir[c])
 };
 
 // dynamic shared memory carve-up
@@ -683,13 +689,16 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
         if (ue < (unsigned)R3) {
             const unsigned up = ue ^ dm;
             EIK_CHECK(up < (unsigned)R3, "wavefront point index");
-            if (lds_u8(ab + up)) {
+            // the flag and the seven box values are loaded together (one shared-memory round
+            // trip on the step's critical path instead of two)
+            const uint32_t qa = vb + EIK_QOFF(up);
+            const uint32_t fl = lds_u8(ab + up);
+            const T v = lds<T>(qa);
+            const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
+            const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
+            const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
+            if (fl) {
                 sts_u8(ab + up, 0u);                                   // Alg. 2 line 4
-                const uint32_t qa = vb + EIK_QOFF(up);
-                const T v = lds<T>(qa);
-                const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
-                const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
-                const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
                 const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
                 const T hf = fabs(hs);
                 if (hf < INF && fmin(mx, fmin(my, mz)) < v) {          // fixed / no gain
@@ -771,7 +780,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     const int64_t base = (int64_t)c * R3;
     if (tid < 6) S.face_min[tid] = KEY_INF;
     if (tid == 0) {
-        S.face_flag = 0; S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
+        S.face_flag = 0;
+        S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
         S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
     }
@@ -902,9 +912,23 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // so its set of active planes is collected here (no separate scan) ----
     __syncthreads();
     if (tid == 0) S.tm[2] = clock64();
-    const int dir0 = (init || !(flags & 63u)) ? 0 :
+    // Sweep-direction state.  A continuation after a sweep cap resumes the direction sequence
+    // where the capped processing left it (the saved word holds the direction chosen for the
+    // sweep it did not run, the Gray-cycle position and the age of each axis' last reversal);
+    // restarting from the inflow faces would repeat the same first sweeps every processing.
+    int gi = 0, lf0 = -64, lf1 = -64, lf2 = -64;   // lfX: sweep of axis X's last reversal
+    const uint32_t dsave = (flags & FLAG_CONT) ? __ldcg(&A.pdir[c]) : 0u;
+    const bool resumed = dsave >> 31;
+    int dir0 = (init || !(flags & 63u)) ? 0 :
         (((flags & 2u) && !(flags & 1u) ? 1 : 0) | ((flags & 8u) && !(flags & 4u) ? 2 : 0) |
          ((flags & 32u) && !(flags & 16u) ? 4 : 0));
+    if (resumed) {
+        dir0 = (int)(dsave & 7u);
+        gi = (int)((dsave >> 3) & 7u);
+        lf0 = -(int)((dsave >> 9) & 63u);
+        lf1 = -(int)((dsave >> 15) & 63u);
+        lf2 = -(int)((dsave >> 21) & 63u);
+    }
     {
         int cnt = 0;
         unsigned long long pm0 = 0;
@@ -963,8 +987,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     __syncthreads();
     if (tid == 0) S.tm[3] = clock64();
 
-    int gi = 0, prev_dir = -1;
-    int lf0 = -1, lf1 = -1, lf2 = -1;   // sweep at which each axis was last reversed
+    int prev_dir = -1;
     bool ran_list = false;
     uint32_t nsweeps = 0;
     uint32_t nupd = 0, nwr = 0;
@@ -1067,7 +1090,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             if (tid == 0) S.bwd[sw & 1] = 0;
             if (prev_dir < 0) {
                 dir = dir0;
-                if (init || !(flags & 63u)) gi = 1;
+                if (!resumed && (init || !(flags & 63u))) gi = 1;
             } else if (bw) {
                 // flip one of those axes per sweep, the least recently flipped one (a source
                 // inside the cell needs all 8 octants: this then walks a Gray cycle)
@@ -1137,7 +1160,12 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             }
             for (int o = 16; o > 0; o >>= 1) km = min(km, __shfl_xor_sync(0xffffffffu, km, o));
             if ((tid & 31) == 0) atomicMin(&S.cont_key, km);
-            if (tid == 0) S.cont = 1;
+            if (tid == 0) {
+                S.cont = 1;
+                auto age = [&](int l) { return (uint32_t)(sw - l < 63 ? sw - l : 63); };
+                S.dstate = (1u << 31) | (uint32_t)dir | ((uint32_t)gi << 3) | (age(lf0) << 9) |
+                           (age(lf1) << 15) | (age(lf2) << 21);
+            }
             break;
         }
         ++nsweeps;
@@ -1340,6 +1368,7 @@ k_cell(CellArgs A)
         cell_process<T, R, true>(A, S, Msm, c, flags, nsw);
         __syncthreads();
         // re-activate currently-downwind neighbour cells (Alg. 1 lines 7-10)
+        if (S.cont && tid == 7) __stcg(&A.pdir[c], S.dstate);   // read in a later round
         if (tid < 6 && (S.face_flag & (1u << tid))) {
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
@@ -1496,6 +1525,10 @@ k_async(CellArgs A)
         cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
         __threadfence();   // value stores before the re-activations
         __syncthreads();
+        if (S.cont && tid == 7) {
+            __stcg(&A.pdir[c], S.dstate);
+            __threadfence();   // before the cell is re-queued below
+        }
         if (tid < 6 && (S.face_flag & (1u << tid))) {
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {

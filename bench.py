@@ -229,6 +229,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--bin-width", type=float, default=None)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--method", default="hcm", choices=["hcm", "dfsm", "dlsm"],
+                    help="hcm: the product path (eik_solve); dfsm / dlsm: the paper's comparison "
+                         "sweeping methods on the GPU (eik_solve_sweep, SURVEY 8(f) F2)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -258,8 +261,16 @@ def main():
     U = torch.empty_like(F)
     stream = torch.cuda.current_stream(dev)
 
+    sweep = args.method != "hcm"
+
+    def run_once():
+        if sweep:
+            solver.solve_sweep(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U, method=args.method)
+        else:
+            solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
+
     for _ in range(args.warmup):
-        solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
+        run_once()
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
@@ -267,7 +278,7 @@ def main():
     with Clocks(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
+            run_once()
             stats.append(solver.stats())
         ev1.record(stream)
         barrier()
@@ -282,20 +293,22 @@ def main():
     peak, peak_src = peaks()
     achieved = alg_bytes / (cell_ms * 1e-3) / 1e9 if cell_ms > 0 else None
     # event-timed cross-check of the same kernel (host-loop mode, CUDA events around launches)
-    s2 = eik.Solver(device=local, loop_mode=1, bin_width=args.bin_width)
-    s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
-    s2.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=torch.empty_like(F))
-    st2 = s2.stats()
-    s2.close()
+    st2 = {"ms_cell_events": 0.0, "cell_launches": 1}
+    if not sweep:
+        s2 = eik.Solver(device=local, loop_mode=1, bin_width=args.bin_width)
+        s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
+        s2.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=torch.empty_like(F))
+        st2 = s2.stats()
+        s2.close()
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"ncu_{args.config}.json")
-    if os.path.exists(tp):   # ncu DRAM bytes of the cell kernel per processing x processings/launch
+    if os.path.exists(tp) and not sweep:   # ncu DRAM bytes of the cell kernel per processing x processings/launch
         d = json.load(open(tp))["kcell_traffic"]
         traffic = d["dram_bytes_per_processing"] * (stats[-1]["cell_processings"] / max(launches, 1))
     st = stats[-1]
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": f"k_cell<{'float' if prec == 'f32' else 'double'},{r}>",
+            "kernel": f"{'k_dsweep' if sweep else 'k_cell'}<{'float' if prec == 'f32' else 'double'},{r}>",
             "alg_bytes_per_launch": alg_bytes / max(launches, 1),
             "ms_per_launch_device": cell_ms / max(launches, 1),
             "ms_per_launch_events": (st2["ms_cell_events"] / max(st2["cell_launches"], 1)),
@@ -304,7 +317,7 @@ def main():
 
     # e2e: the same solve through the C ABI with pinned HOST buffers, copies inside the timing
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and not sweep:
         Fh = F.cpu().pin_memory()
         mh = m.cpu().pin_memory()
         qh = q.cpu().pin_memory()
@@ -332,11 +345,17 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
-            "config": config_block(cfg, prec, r, n),
+            "config": dict(config_block(cfg, prec, r, n), **({"solve": f"eik_solve_sweep ({args.method}): "
+                           "ingest + whole-grid sweep loop (CUDA graph) + egress"} if sweep else {})),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(args.steps * (4 + 3 * rounds)),
+            # per solve: init, ingest, (worklist build), egress + the loop's launches: fused
+            # rounds = one k_cell each (k_select + k_cell + k_round_end otherwise); sweeping =
+            # one k_dsweep per cell diagonal + k_sweep_end per sweep
+            "gpu_launches": int(args.steps * (4 + (launches + rounds if sweep else
+                                                   rounds * (1 if args.bin_width is None else 3)))),
             "clocks": clk.summary(),
-            "work": {"rounds": st["rounds"], "cell_processings": st["cell_processings"],
+            "method": args.method,
+            "work": {"rounds": st["rounds"], "grid_sweeps": st["grid_sweeps"], "cell_processings": st["cell_processings"],
                      "processings_per_cell": st["cell_processings"] / st["J"],
                      "sweeps_per_cell": st["cell_sweeps"] / st["J"],
                      "updates_per_point": st["point_updates"] / st["M"],

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EIK_ABI_VERSION 1
+#define EIK_ABI_VERSION 2
 
 typedef struct eik_ctx eik_ctx;
 
@@ -42,6 +42,7 @@ typedef enum {
 } eik_status;
 
 typedef enum { EIK_F32 = 0, EIK_F64 = 1 } eik_precision;
+typedef enum { EIK_DFSM = 0, EIK_DLSM = 1 } eik_sweep_method;   /* eik_solve_sweep */
 
 /* Options for eik_set_option (all optional; defaults in brackets). */
 typedef enum {
@@ -93,7 +94,10 @@ typedef struct {
                                    start to last CTA end, %globaltimer), any loop mode          */
     double   ms_cell_events;    /* sum of CUDA-event durations of the cell-sweep launches
                                    (EIK_OPT_TIME_CELL_EVENTS in host loop mode), else 0         */
-    uint64_t cell_launches;     /* cell-sweep kernel launches that processed >= 1 cell        */
+    uint64_t cell_launches;     /* cell-sweep kernel launches that processed >= 1 cell
+                                   (eik_solve_sweep: diagonal launches)                         */
+    uint64_t grid_sweeps;       /* eik_solve_sweep: whole-grid sweeps, the last of which changed
+                                   nothing (the FSM count of P:803, Table 4); else 0            */
 } eik_stats;
 
 /* Create a context on `device`.  cuda_stream: a cudaStream_t to enqueue on (e.g. torch's
@@ -129,6 +133,21 @@ int eik_solve(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* e
  * inputs and the device->host copy of U happen inside the call (the e2e path). */
 int eik_solve_host(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
                    const void* exit_vals, void* U_out, int precision, int cell_size);
+
+/* Whole-grid sweeping: the paper's comparison methods (P:140-149 FSM / LSM, P:175-186
+ * Detrixhe's DFSM, P:795-801 DLSM) on the same device tiles, same contract
+ * and arguments as eik_solve plus
+ *   method     EIK_DFSM: Gauss-Seidel sweeps of Eq. (2) in the 2^3 directions, sweep s in
+ *              direction s mod 8 (bit 0/1/2 = x/y/z descending), until a sweep changes
+ *              nothing (counted).  The ordering is a cell-diagonal wavefront with a
+ *              point-plane wavefront inside each cell: the same values after every sweep as
+ *              the lexicographic FSM, hence the same sweep count.
+ *              EIK_DLSM: DFSM that skips a cell whose inputs did not change since it last
+ *              ran (locking at cell granularity): same values and sweep count as DFSM.
+ * The sweep count is eik_stats.grid_sweeps; EIK_OPT_MAX_ROUNDS caps it (EIK_EINTERNAL).
+ * EIK_EINVAL additionally for an unknown method. */
+int eik_solve_sweep(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
+                    const void* exit_vals, void* U_out, int precision, int cell_size, int method);
 
 /* Stats of the last successful solve.  EIK_EINVAL if ctx/out is NULL. */
 int eik_get_stats(const eik_ctx* ctx, eik_stats* out);

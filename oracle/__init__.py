@@ -50,6 +50,8 @@ def _load():
         lib.orc_check.restype = None
         lib.orc_residual_ratio.argtypes = [I64, D, P, P, P, D, D, P]
         lib.orc_residual_ratio.restype = D
+        lib.orc_fsm.argtypes = [I64, D, P, P, P, P, ctypes.c_int, I64, P]
+        lib.orc_fsm.restype = I64
         _lib = lib
     return _lib
 
@@ -95,6 +97,23 @@ def value_iteration(n: int, F, exit_mask, exit_vals, h: float | None = None,
     if it < 0:
         raise RuntimeError(f"orc_value_iteration status {it}")
     return (U, it) if return_iters else U
+
+
+def fsm(n: int, F, exit_mask, exit_vals, h: float | None = None, lsm: bool = False,
+        max_sweeps: int = 100000):
+    """Serial fp64 Fast Sweeping (lsm=True: Locking Sweeping).  Returns
+    (U, sweeps, local solves); sweep s runs direction s mod 8 (bit 0/1/2 = i/j/k descending)
+    and the last sweep changes nothing."""
+    lib = _load()
+    h = 1.0 / n if h is None else h
+    F_, m_, q_ = _c64(F), _cu8(exit_mask), _c64(exit_vals)
+    U = np.empty_like(F_)
+    upd = ctypes.c_int64(0)
+    s = lib.orc_fsm(n, h, _ptr(F_), _ptr(m_), _ptr(q_), _ptr(U), int(lsm), max_sweeps,
+                    ctypes.byref(upd))
+    if s < 0:
+        raise RuntimeError(f"orc_fsm status {s}")
+    return U, int(s), int(upd.value)
 
 
 def bfs(n: int, F, exit_mask):

@@ -30,6 +30,14 @@
  *                        F > 0 points (the finite-iff-reachable contract, C.6, R11).
  *   orc_check            invariant checkers on any candidate solution U (C.5/C.6):
  *                        Eq. (2) residual, discrete Lipschitz bound, causal parent.
+ *   orc_fsm              the Fast Sweeping Method: Gauss-Seidel sweeps of Eq. (2)
+ *                        in the 2^3 standard loop orderings, alternated, until a sweep changes
+ *                        nothing; with lsm = 1 the Locking Sweeping Method: a point
+ *                        is updated only while "active" (initially the neighbours of the exit
+ *                        set; a change activates the neighbours).  Pinned by: the paper's sweep
+ *                        count of Ex. 1 (9 at every M, Table 4), LSM = FSM sweeps and
+ *                        values, the FSM fixed point = FMM / value iteration on random
+ *                        grids (tests/test_oracle_fsm.py).
  */
 #include <math.h>
 #include <stdint.h>
@@ -391,4 +399,77 @@ double orc_residual_ratio(int64_t n, double h, const double* F, const uint8_t* m
     }
     if (at) *at = wat;
     return worst;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Fast Sweeping Method: Gauss-Seidel iteration of
+ *   V_p <- min(V_p, solve(minima(V)))   (non-exit points with F_p > 0)
+ * over the gridpoints in one of the 2^3 standard loop orderings per sweep ("sweep
+ * directions").  Sweep s uses direction d = s mod 8 (bit 0: i descending, bit 1:
+ * j descending, bit 2: k descending; k outermost, i innermost).  Sweeps continue as long as
+ * some gridpoint received an updated value: the last sweep changes nothing and is
+ * counted (Ex. 1 converges in 8 + 1 = 9 sweeps, Table 4).
+ * lsm = 1: Locking Sweeping Method: active flags, initially set at the non-exit
+ * neighbours of the exit set; a point is relaxed only if active, its flag is cleared when it
+ * is relaxed, and a changed value activates its neighbours (a value cannot change unless a
+ * neighbour changed since its last update).
+ * Returns the number of sweeps, -1 if max_sweeps was reached, -2 on allocation failure;
+ * *n_updates (if not NULL) = local solves performed.
+ * ------------------------------------------------------------------------------------- */
+int64_t orc_fsm(int64_t n, double h, const double* F, const uint8_t* mask, const double* q,
+                double* V, int lsm, int64_t max_sweeps, int64_t* n_updates)
+{
+    grid_t g = { n + 1, (n + 1) * (n + 1) * (n + 1) };
+    int64_t n1 = g.n1;
+    uint8_t* act = NULL;
+    for (int64_t p = 0; p < g.M; ++p) V[p] = mask[p] ? q[p] : ORC_INF;
+    if (lsm) {
+        act = (uint8_t*)calloc((size_t)g.M, 1);
+        if (!act) return -2;
+        for (int64_t p = 0; p < g.M; ++p) {
+            if (!mask[p]) continue;
+            int64_t nb[6];
+            int c = neighbours(&g, p, nb);
+            for (int a = 0; a < c; ++a) if (!mask[nb[a]]) act[nb[a]] = 1;
+        }
+    }
+    int64_t upd = 0, s = 0;
+    for (;;) {
+        if (s >= max_sweeps) { free(act); return -1; }
+        int d = (int)(s % 8);
+        s++;
+        int changed = 0;
+        for (int64_t kk = 0; kk < n1; ++kk) {
+            int64_t k = (d & 4) ? n1 - 1 - kk : kk;
+            for (int64_t jj = 0; jj < n1; ++jj) {
+                int64_t j = (d & 2) ? n1 - 1 - jj : jj;
+                for (int64_t ii = 0; ii < n1; ++ii) {
+                    int64_t i = (d & 1) ? n1 - 1 - ii : ii;
+                    int64_t p = gidx(&g, i, j, k);
+                    if (mask[p] || !(F[p] > 0.0)) continue;
+                    if (lsm) {
+                        if (!act[p]) continue;
+                        act[p] = 0;
+                    }
+                    double m[3];
+                    axis_minima(&g, V, p, m);
+                    upd++;
+                    double u = orc_solve_local(m[0], m[1], m[2], h / F[p]);
+                    if (u < V[p]) {
+                        V[p] = u;
+                        changed = 1;
+                        if (lsm) {
+                            int64_t nb[6];
+                            int c = neighbours(&g, p, nb);
+                            for (int a = 0; a < c; ++a) act[nb[a]] = 1;
+                        }
+                    }
+                }
+            }
+        }
+        if (!changed) break;
+    }
+    free(act);
+    if (n_updates) *n_updates = upd;
+    return s;
 }

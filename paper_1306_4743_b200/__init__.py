@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("EIK_LIB") or os.path.join(
 
 EIK_OK, EIK_EINVAL, EIK_ENOMEM, EIK_ECUDA, EIK_ENOTSUP, EIK_EINTERNAL = range(6)
 EIK_F32, EIK_F64 = 0, 1
+EIK_DFSM, EIK_DLSM = 0, 1          # eik_solve_sweep methods
 (EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS,
  EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS, EIK_OPT_TIMEOUT_S) = range(8)
 STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
@@ -26,7 +27,8 @@ STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
 
 # every symbol include/eik.h declares (checked by tests/test_abi.py)
 EXPORTS = ("eik_create", "eik_set_stream", "eik_set_option", "eik_solve", "eik_solve_host",
-           "eik_get_stats", "eik_get_debug", "eik_last_error", "eik_destroy", "eik_abi_version")
+           "eik_solve_sweep", "eik_get_stats", "eik_get_debug", "eik_last_error", "eik_destroy",
+           "eik_abi_version")
 
 
 class EikStats(ctypes.Structure):
@@ -41,7 +43,7 @@ class EikStats(ctypes.Structure):
                 ("ms_ingest", ctypes.c_double), ("ms_loop", ctypes.c_double),
                 ("ms_egress", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("ms_cell_device", ctypes.c_double), ("ms_cell_events", ctypes.c_double),
-                ("cell_launches", ctypes.c_uint64)]
+                ("cell_launches", ctypes.c_uint64), ("grid_sweeps", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
@@ -68,6 +70,8 @@ def _load():
     for f in (lib.eik_solve, lib.eik_solve_host):
         f.argtypes = [P, I64, D, P, P, P, P, I, I]
         f.restype = I
+    lib.eik_solve_sweep.argtypes = [P, I64, D, P, P, P, P, I, I, I]
+    lib.eik_solve_sweep.restype = I
     lib.eik_get_stats.argtypes = [P, ctypes.POINTER(EikStats)]
     lib.eik_get_stats.restype = I
     lib.eik_get_debug.argtypes = [P, P, I]
@@ -151,6 +155,33 @@ class Solver:
         lib.eik_set_stream(self._ctx, ctypes.c_void_p(stream))
         st = lib.eik_solve(self._ctx, n, h, F.data_ptr(), exit_mask.data_ptr(),
                            exit_vals.data_ptr(), out.data_ptr(), prec, cell_size)
+        if st != EIK_OK:
+            raise self._err(st)
+        return out
+
+    def solve_sweep(self, F, exit_mask, exit_vals, h: float | None = None, cell_size: int = 16,
+                    method: str = "dfsm", n: int | None = None, out=None):
+        """The paper's comparison methods on the device (eik_solve_sweep): whole-grid
+        Gauss-Seidel sweeping, method "dfsm" (Detrixhe FSM) or "dlsm" (locking,
+        P:148-149).  Same tensor contract as solve(); the sweep count is
+        stats()["grid_sweeps"]."""
+        import torch
+        m = {"dfsm": EIK_DFSM, "dlsm": EIK_DLSM}[method]
+        if F.dtype not in (torch.float32, torch.float64):
+            raise TypeError("F must be float32 or float64")
+        prec = EIK_F32 if F.dtype == torch.float32 else EIK_F64
+        for t in (F, exit_mask, exit_vals):
+            if not (t.is_cuda and t.is_contiguous()):
+                raise ValueError("solve_sweep() takes contiguous CUDA tensors")
+        if exit_mask.dtype != torch.uint8 or exit_vals.dtype != F.dtype:
+            raise TypeError("exit_mask must be uint8 and exit_vals must have F's dtype")
+        n = _n_from_numel(F.numel()) if n is None else n
+        h = 1.0 / n if h is None else h
+        if out is None:
+            out = torch.empty_like(F)
+        lib.eik_set_stream(self._ctx, ctypes.c_void_p(torch.cuda.current_stream(F.device).cuda_stream))
+        st = lib.eik_solve_sweep(self._ctx, n, h, F.data_ptr(), exit_mask.data_ptr(),
+                                 exit_vals.data_ptr(), out.data_ptr(), prec, cell_size, m)
         if st != EIK_OK:
             raise self._err(st)
         return out

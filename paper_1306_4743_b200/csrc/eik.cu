@@ -59,9 +59,17 @@ struct eik_ctx {
     // host-pointer staging (eik_solve_host)
     void* stage = nullptr;
     size_t stage_bytes = 0;
-    // graph cache
+    // graph cache (scheduler loop; whole-grid sweep loop)
     cudaGraphExec_t gexec = nullptr;
     std::string gkey;
+    cudaGraphExec_t gexec_sw = nullptr;
+    std::string gkey_sw;
+    // whole-grid sweeping: cells grouped by canonical diagonal (per cps), DLSM cell flags
+    uint32_t* diag_cells = nullptr;
+    uint32_t* diag_off = nullptr;
+    int diag_cps = 0;
+    std::vector<uint32_t> diag_off_h;
+    uint8_t* cact = nullptr;
     // events
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     eik_stats stats{};
@@ -172,6 +180,14 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     CK(cudaFuncSetAttribute(k_async<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 8>()));
     CK(cudaFuncSetAttribute(k_async<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 4>()));
     CK(cudaFuncSetAttribute(k_async<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 4>()));
+    CK(cudaFuncSetAttribute(k_dsweep<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
+    CK(cudaFuncSetAttribute(k_dsweep<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 16>()));
+    CK(cudaFuncSetAttribute(k_dsweep<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 8>()));
+    CK(cudaFuncSetAttribute(k_dsweep<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 8>()));
+    CK(cudaFuncSetAttribute(k_dsweep<float, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 4>()));
+    CK(cudaFuncSetAttribute(k_dsweep<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 4>()));
+    CK(cudaFuncSetAttribute(k_dsweep<float, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaFuncSetAttribute(k_dsweep<double, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     *out = ctx;
     return EIK_OK;
 }
@@ -181,6 +197,10 @@ static void free_scratch(eik_ctx* ctx)
     cudaFree(ctx->Vt); cudaFree(ctx->Ht);
     cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
     cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen); cudaFree(ctx->pdir);
+    cudaFree(ctx->diag_cells); cudaFree(ctx->diag_off); cudaFree(ctx->cact);
+    ctx->diag_cells = ctx->diag_off = nullptr;
+    ctx->cact = nullptr;
+    ctx->diag_cps = 0;
     ctx->pend = nullptr;
     ctx->pdir = nullptr;
     ctx->gen = nullptr;
@@ -195,6 +215,7 @@ extern "C" void eik_destroy(eik_ctx* ctx)
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->gexec_sw) cudaGraphExecDestroy(ctx->gexec_sw);
     free_scratch(ctx);
     cudaFree(ctx->stage);
     cudaFree(ctx->ctl);
@@ -295,6 +316,7 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
 {
     if (tile_bytes > ctx->tile_bytes || J > ctx->cell_cap) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; ctx->gkey.clear(); }
+        if (ctx->gexec_sw) { cudaGraphExecDestroy(ctx->gexec_sw); ctx->gexec_sw = nullptr; ctx->gkey_sw.clear(); }
         CK(cudaStreamSynchronize(ctx->stream));
         free_scratch(ctx);
         CK(cudaMalloc(&ctx->Vt, tile_bytes));
@@ -312,6 +334,8 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
         CK(cudaMalloc(&ctx->pend, J * 512));   // R^3 / 8 bytes per cell at r = 16
         CK(cudaMalloc(&ctx->pdir, J * 4));     // sweep-direction state at a cap
         CK(cudaMalloc(&ctx->gen, J * 4));
+        CK(cudaMalloc(&ctx->diag_cells, J * 4));
+        CK(cudaMalloc(&ctx->cact, J));
         ctx->cell_cap = J;
     }
     return EIK_OK;
@@ -485,9 +509,128 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
     return EIK_OK;
 }
 
+// ---- whole-grid sweeping: DFSM / DLSM on the cell tiles ----------------
+// end of one sweep: count it, stop after the first sweep that changed nothing (the
+// FSM convention the paper's sweep counts use), or at the sweep cap / watchdog
+__global__ void k_sweep_end(Ctl* ctl, cudaGraphConditionalHandle h)
+{
+    volatile Ctl* c = ctl;
+    const unsigned long long w = c->sweep_writes;
+    c->sweep_idx += 1;
+    c->rounds += 1;
+    c->sweep_writes = 0;
+    bool more = w != 0;
+    if (more && c->sweep_idx >= c->max_rounds) { c->err |= 4u; more = false; }
+    if (more && gtimer() - c->t_solve0 > c->budget_ns) { c->err |= 8u; more = false; }
+    cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
+// cells grouped by canonical diagonal a + b + c = D (one table serves all 8 directions: a
+// direction reflects the canonical coordinates)
+static int ensure_diag(eik_ctx* ctx, int cps)
+{
+    if (ctx->diag_cps == cps) return EIK_OK;
+    const int nd = 3 * cps - 2;
+    std::vector<uint32_t> cells;
+    cells.reserve((size_t)cps * cps * cps);
+    ctx->diag_off_h.assign(nd + 1, 0);
+    for (int D = 0; D < nd; ++D) {
+        ctx->diag_off_h[D] = (uint32_t)cells.size();
+        for (int c = 0; c < cps; ++c)
+            for (int b = 0; b < cps; ++b) {
+                const int a = D - b - c;
+                if (a >= 0 && a < cps) cells.push_back((uint32_t)a + (uint32_t)cps * ((uint32_t)b + (uint32_t)cps * (uint32_t)c));
+            }
+    }
+    ctx->diag_off_h[nd] = (uint32_t)cells.size();
+    cudaFree(ctx->diag_off);
+    ctx->diag_off = nullptr;
+    CK(cudaMalloc(&ctx->diag_off, (size_t)(nd + 1) * 4));
+    CK(cudaMemcpy(ctx->diag_off, ctx->diag_off_h.data(), (size_t)(nd + 1) * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->diag_cells, cells.data(), cells.size() * 4, cudaMemcpyHostToDevice));
+    ctx->diag_cps = cps;
+    return EIK_OK;
+}
+
+template <typename T, int R>
+static int sweep_grid_r(eik_ctx* ctx, int* grid)
+{
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dsweep<T, R>, CellCfg<R>::NT, cell_smem_bytes<T, R>()));
+    *grid = (occ < 1 ? 1 : occ) * ctx->sm_count;
+    return EIK_OK;
+}
+
+template <typename T, int R>
+static int capture_sweep(eik_ctx* ctx, const CellArgs& ca, int cps, cudaStream_t cs, int maxgrid)
+{
+    for (int D = 0; D < 3 * cps - 2; ++D) {
+        const int cnt = (int)(ctx->diag_off_h[D + 1] - ctx->diag_off_h[D]);
+        const int grid = cnt < maxgrid ? cnt : maxgrid;
+        k_dsweep<T, R><<<grid, CellCfg<R>::NT, cell_smem_bytes<T, R>(), cs>>>(ca, D);
+        CK(cudaGetLastError());
+    }
+    return EIK_OK;
+}
+
+// the whole sweep loop is one CUDA graph: WHILE (the last sweep changed something) { one
+// launch per cell diagonal; k_sweep_end } -- no host round-trip per sweep
+template <typename T>
+static int run_sweeps(eik_ctx* ctx, int r, int64_t J, CellArgs ca, int method)
+{
+    const int cps = ca.cps;
+    int st = ensure_diag(ctx, cps);
+    if (st) return st;
+    ca.diag_cells = ctx->diag_cells;
+    ca.diag_off = ctx->diag_off;
+    ca.cact = ctx->cact;
+    ca.locked = method == EIK_DLSM ? 1 : 0;
+    CK(cudaMemsetAsync(ctx->cact, 1, (size_t)J, ctx->stream));   // the first sweep relaxes everything
+    int maxgrid = 0;
+    st = r == 16 ? sweep_grid_r<T, 16>(ctx, &maxgrid) : r == 8 ? sweep_grid_r<T, 8>(ctx, &maxgrid)
+                                                               : sweep_grid_r<T, 4>(ctx, &maxgrid);
+    if (st) return st;
+    char keybuf[256];
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%d/%d", (int)sizeof(T), r, (long long)J,
+             (long long)ca.n1, ca.Vt, ca.Ht, ca.stats, ca.locked);
+    if (!ctx->gexec_sw || ctx->gkey_sw != keybuf) {
+        if (ctx->gexec_sw) { cudaGraphExecDestroy(ctx->gexec_sw); ctx->gexec_sw = nullptr; }
+        cudaGraph_t graph;
+        CK(cudaGraphCreate(&graph, 0));
+        cudaGraphConditionalHandle handle;
+        CK(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = handle;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cnode;
+        CK(cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        st = r == 16 ? capture_sweep<T, 16>(ctx, ca, cps, cs, maxgrid)
+           : r == 8 ? capture_sweep<T, 8>(ctx, ca, cps, cs, maxgrid)
+                    : capture_sweep<T, 4>(ctx, ca, cps, cs, maxgrid);
+        k_sweep_end<<<1, 1, 0, cs>>>(ctx->ctl, handle);
+        cudaGraph_t captured;
+        cudaError_t ce = cudaStreamEndCapture(cs, &captured);
+        cudaStreamDestroy(cs);
+        if (st) { cudaGraphDestroy(graph); return st; }
+        if (ce != cudaSuccess) { cudaGraphDestroy(graph); CK(ce); }
+        cudaError_t ie = cudaGraphInstantiate(&ctx->gexec_sw, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ie);
+        ctx->gkey_sw = keybuf;
+    }
+    CK(cudaGraphLaunch(ctx->gexec_sw, ctx->stream));
+    return EIK_OK;
+}
+
 template <typename T>
 static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* mask,
-                      const void* q, void* U, int r)
+                      const void* q, void* U, int r, int method)
 {
     const int64_t n1 = n + 1;
     const int cps = (int)((n1 + r - 1) / r);
@@ -519,7 +662,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
         k_ingest<T><<<dim3(bx, by), 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt,
                                                  (T*)ctx->Ht, ctx->key, ctx->state, ctx->ctl, P);
     }
-    if (ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
+    if (method < 0 && ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
     // input validation result (device-detected errors return before touching U_out)
     CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
@@ -551,7 +694,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.cps = cps;
     ca.stats = ctx->collect_stats;
     ca.fused = isinf(ctx->bin_width) ? 1 : 0;
-    st = run_loop<T>(ctx, r, J, ca);
+    st = method < 0 ? run_loop<T>(ctx, r, J, ca) : run_sweeps<T>(ctx, r, J, ca, method);
     if (st) return st;
     CK(cudaEventRecord(ctx->ev[2], s));
     // host-side guard against a device loop that never returns (the device watchdog covers
@@ -585,7 +728,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (ctx->ctl_host->err & 4u)
-        return fail(ctx, EIK_EINTERNAL, "max rounds (%u) exceeded", ctx->max_rounds);
+        return fail(ctx, EIK_EINTERNAL, "max %s (%u) exceeded", method < 0 ? "rounds" : "sweeps", ctx->max_rounds);
     if (ctx->ctl_host->err & 8u)
         return fail(ctx, EIK_EINTERNAL, "watchdog: solve exceeded %.1f s (pending %u head %u tail %u "
                     "rounds %u processings %llu)", ctx->timeout_s, ctx->ctl_host->pending,
@@ -630,6 +773,11 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     S.ms_cell_device = hc.cell_ns * 1e-6;
     S.ms_cell_events = ctx->ms_cell_events;
     S.cell_launches = hc.cell_launches;
+    if (method >= 0) {
+        S.grid_sweeps = hc.sweep_idx;
+        S.cell_launches = (uint64_t)hc.sweep_idx * (uint64_t)(3 * cps - 2);
+        S.ms_cell_device = S.ms_loop;
+    }
     ctx->have_stats = true;
     return EIK_OK;
 }
@@ -655,8 +803,20 @@ extern "C" int eik_solve(eik_ctx* ctx, int64_t n, double h, const void* F, const
     if (st) return st;
     CK(cudaSetDevice(ctx->device));
     ctx->have_stats = false;
-    if (precision == EIK_F32) return solve_impl<float>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size);
-    return solve_impl<double>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size);
+    if (precision == EIK_F32) return solve_impl<float>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size, -1);
+    return solve_impl<double>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size, -1);
+}
+
+extern "C" int eik_solve_sweep(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,
+                               const void* exit_vals, void* U_out, int precision, int cell_size, int method)
+{
+    int st = validate(ctx, n, h, F, exit_mask, exit_vals, U_out, precision, cell_size);
+    if (st) return st;
+    if (method != EIK_DFSM && method != EIK_DLSM) return fail(ctx, EIK_EINVAL, "bad sweep method %d", method);
+    CK(cudaSetDevice(ctx->device));
+    ctx->have_stats = false;
+    if (precision == EIK_F32) return solve_impl<float>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size, method);
+    return solve_impl<double>(ctx, n, h, F, exit_mask, exit_vals, U_out, cell_size, method);
 }
 
 extern "C" int eik_solve_host(eik_ctx* ctx, int64_t n, double h, const void* F, const uint8_t* exit_mask,

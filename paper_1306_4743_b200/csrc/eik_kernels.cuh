@@ -213,6 +213,9 @@ struct Ctl {
     // diagnostics (eik_get_debug): [0] sum of per-processing SM cycles, [1] max, [2] plane
     // steps executed, [3] processings, [4..35] histogram of sweeps per processing (31 = >=31)
     unsigned long long dbg[43];   // [36] stage, [37] plane-mask, [38] steps, [39] write-back cycles, [40] list iterations
+    // whole-grid sweeping (k_dsweep): sweep s runs direction s mod 8
+    uint32_t sweep_idx;           // sweeps completed
+    unsigned long long sweep_writes;   // strict decreases in the current sweep
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -526,6 +529,11 @@ struct CellArgs {
     uint32_t cap;                    // number of cells J (bounds checks)
     uint32_t* pend;                  // J x R^3/32 saved active bits (FLAG_CONT)
     uint32_t* pdir;                  // J: sweep-direction state saved at a sweep cap (FLAG_CONT)
+    // whole-grid sweeping (k_dsweep)
+    const uint32_t* diag_cells;      // canonical cells a + cps (b + cps c), grouped by a + b + c
+    const uint32_t* diag_off;        // [3 cps - 1]: start of each cell diagonal in diag_cells
+    uint8_t* cact;                   // DLSM: cell has an input that changed since it last ran
+    int32_t locked;                  // 1: DLSM (skip cells whose inputs did not change)
     int32_t fused;                   // round mode, bin width +inf: k_cell takes its cells straight
                                      // from the current worklist (the whole list is selected) and
                                      // its last CTA ends the round (no k_select / k_round_end)
@@ -736,6 +744,100 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     return bwd;
 }
 
+// Stage cell c (tile coordinates cx, cy, cz) into shared memory: the tile and its hf go out
+// as cp.async (no registers), the halo N(c) as L2 loads issued right behind them -- one
+// memory round trip for all of it; returns when this thread's copies have landed (the caller
+// synchronises the CTA).  The tile's element-wise copies (into the padded box) use .ca, which
+// is safe for the cell's own tile: no other CTA writes it within a launch, and L1 does not
+// survive the kernel boundary.  The halo must come from L2 (.cg): a neighbour processed
+// earlier in this launch on another SM may have changed it after this SM cached the lines.
+template <typename T, int R>
+__device__ __forceinline__ void stage_cell_async(const T* __restrict__ Vt, const T* __restrict__ Ht,
+                                                 T* sV, T* sH, uint32_t c, int cx, int cy, int cz,
+                                                 int cps, uint32_t cap)
+{
+    using C = CellCfg<R>;
+    constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2;
+    const int tid = threadIdx.x;
+    const T INF = dinf<T>();
+    const int64_t base = (int64_t)c * R3;
+    (void)cap;
+    const uint32_t vs = smem_u32(sV), hs = smem_u32(sH);
+    constexpr int EL = 16 / sizeof(T);
+    for (int vi = tid; vi < R3 / EL; vi += NT) cp_async16(hs + vi * 16, Ht + base + vi * EL);
+    for (int e = tid; e < R3; e += NT) {
+        const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+        cp_async_el(vs + ((a + 1) + RP * (b + 1) + RP2 * (d + 1)) * (int)sizeof(T), Vt + base + e);
+    }
+    constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
+    T hv[PH];
+    int hq[PH];
+#pragma unroll
+    for (int m = 0; m < PH; ++m) {
+        const int e = tid + m * NT;
+        hq[m] = -1;
+        hv[m] = INF;
+        if (e < 6 * R * R) {
+            const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
+            int hx, hy, hz, sa, sb, sd;
+            int64_t nc;
+            bool ex;
+            switch (f) {
+            case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
+            case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
+            case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
+            case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
+            case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
+            default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
+            }
+            hq[m] = (hx + 1) + RP * (hy + 1) + RP2 * (hz + 1);
+            EIK_CHECK(!ex || (nc >= 0 && nc < (int64_t)cap), "halo neighbour cell");
+            if (ex) hv[m] = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < PH; ++m)
+        if (hq[m] >= 0) sV[hq[m]] = hv[m];
+    cp_async_wait_all();
+}
+
+// Write back the changed points of a staged cell (sign bit of hf set): 16-byte vectors, a
+// vector holding any changed point is stored whole (unchanged values are rewritten
+// identically).  Returns the number of changed points this thread wrote.
+template <typename T, int R>
+__device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__ Vc, const T* sV,
+                                                                 const T* sH)
+{
+    using C = CellCfg<R>;
+    constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2;
+    using V4 = typename Vec16<T>::type;
+    constexpr int EL = 16 / sizeof(T);
+    constexpr int NV = R3 / EL;
+    unsigned long long nw = 0;
+    V4* Vt4 = reinterpret_cast<V4*>(Vc);
+    const V4* sH4 = reinterpret_cast<const V4*>(sH);
+    for (int vi = threadIdx.x; vi < NV; vi += NT) {
+        const V4 hv = sH4[vi];
+        const T* ph = reinterpret_cast<const T*>(&hv);
+        int nchg = 0;
+#pragma unroll
+        for (int l = 0; l < EL; ++l) nchg += ph[l] < T(0);
+        if (nchg) {
+            V4 out;
+            T* po = reinterpret_cast<T*>(&out);
+#pragma unroll
+            for (int l = 0; l < EL; ++l) {
+                const int e = vi * EL + l;
+                const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+                po[l] = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
+            }
+            __stcg(&Vt4[vi], out);
+            nw += nchg;
+        }
+    }
+    return nw;
+}
+
 // Process one cell to convergence (HCM "perform modified LSM on c until convergence",
 // Alg. 1 line 6): stage the tile and its one-point halo N(c) (boundary data of
 // c~ = c u N(c)), relax the gated (LSM) update of Alg. 2 until no point is active, write
@@ -796,50 +898,10 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // store: memory-level parallelism), then the halo N(c) ----
     const bool init = flags & FLAG_INIT;
     if constexpr (CPASYNC) {
-        // Round mode: the tile and its hf go out as cp.async (no registers), the halo as
-        // L2 loads issued right behind them -- one memory round trip for all of it.  The
-        // tile's element-wise copies (into the padded box) use .ca, which is safe for the
-        // cell's own tile: no other CTA writes it within a round, and L1 does not survive the
-        // kernel boundary.  The halo must come from L2 (.cg): a neighbour processed earlier in
-        // this round on another SM may have changed it after this SM cached the lines, and its
-        // re-activation of this cell is consumed by this very processing (fused rounds).
-        const uint32_t vs = smem_u32(sV), hs = smem_u32(sH);
-        constexpr int EL = 16 / sizeof(T);
-        for (int vi = tid; vi < R3 / EL; vi += NT) cp_async16(hs + vi * 16, Ht + base + vi * EL);
-        for (int e = tid; e < R3; e += NT) {
-            const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
-            cp_async_el(vs + ((a + 1) + RP * (b + 1) + RP2 * (d + 1)) * (int)sizeof(T), Vt + base + e);
-        }
-        constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
-        T hv[PH];
-        int hq[PH];
-#pragma unroll
-        for (int m = 0; m < PH; ++m) {
-            const int e = tid + m * NT;
-            hq[m] = -1;
-            hv[m] = INF;
-            if (e < 6 * R * R) {
-                const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
-                int hx, hy, hz, sa, sb, sd;
-                int64_t nc;
-                bool ex;
-                switch (f) {
-                case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
-                case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
-                case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
-                case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
-                case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
-                default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
-                }
-                hq[m] = (hx + 1) + RP * (hy + 1) + RP2 * (hz + 1);
-                EIK_CHECK(!ex || (nc >= 0 && nc < (int64_t)A.cap), "halo neighbour cell");
-                if (ex) hv[m] = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
-            }
-        }
-#pragma unroll
-        for (int m = 0; m < PH; ++m)
-            if (hq[m] >= 0) sV[hq[m]] = hv[m];
-        cp_async_wait_all();
+        // Round mode: cp.async staging (see stage_cell_async; a round is one launch, and a
+        // neighbour's re-activation of this cell may be consumed by this very processing in
+        // fused rounds, hence the halo from L2)
+        stage_cell_async<T, R>(Vt, Ht, sV, sH, c, cx, cy, cz, cps, A.cap);
         if (tid == 0) S.tm[1] = clock64();
     } else {
         using V4 = typename Vec16<T>::type;
@@ -1226,33 +1288,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 
     // ---- write back (16-byte vectors; a vector holding any changed point is stored whole,
     // unchanged values are rewritten identically) ----
-    unsigned long long nw = 0;
-    {
-        using V4 = typename Vec16<T>::type;
-        constexpr int EL = 16 / sizeof(T);
-        constexpr int NV = R3 / EL;
-        V4* Vt4 = reinterpret_cast<V4*>(Vt + base);
-        const V4* sH4 = reinterpret_cast<const V4*>(sH);
-        for (int vi = tid; vi < NV; vi += NT) {
-            const V4 hv = sH4[vi];
-            const T* ph = reinterpret_cast<const T*>(&hv);
-            int nchg = 0;
-#pragma unroll
-            for (int l = 0; l < EL; ++l) nchg += ph[l] < T(0);
-            if (nchg) {
-                V4 out;
-                T* po = reinterpret_cast<T*>(&out);
-#pragma unroll
-                for (int l = 0; l < EL; ++l) {
-                    const int e = vi * EL + l;
-                    const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
-                    po[l] = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
-                }
-                __stcg(&Vt4[vi], out);
-                nw += nchg;
-            }
-        }
-    }
+    unsigned long long nw = write_back_changed<T, R>(Vt + base, sV, sH);
     if (A.stats) {
         unsigned long long u64 = nupd, w64 = nwr;
         for (int o = 16; o > 0; o >>= 1) {
@@ -1560,6 +1596,129 @@ k_async(CellArgs A)
         }
     }
     if (tid == 0) atomicMax(&ctl->t_end, gtimer());
+}
+
+// --------------------------------------------------------------------------------------
+// Whole-grid sweeping: the paper's comparison methods on the same tiles.
+// FSM relaxes every gridpoint once per sweep in one of the 2^3 loop orderings;
+// Detrixhe's DFSM visits the planes alpha.(i,j,k) = C of the sweep direction in
+// order, the points of a plane in parallel.  Here the ordering is two-level: the cells of one
+// cell diagonal a + b + c = D (canonical, i.e. reflected per direction) form one launch and
+// run concurrently; inside a cell the CTA visits its point planes in order (sweep_dir).  This
+// is another linear extension of the same dependency order -- when a point is relaxed exactly
+// its upwind neighbours (smaller canonical i, j or k) already hold this sweep's values, in
+// its own cell or in an upwind cell of diagonal D - 1, and its downwind neighbours do not --
+// so every sweep produces the same values as the lexicographic FSM sweep of that direction
+// and the number of sweeps is the FSM's.  DLSM skips work
+// that cannot change anything; here at cell granularity: a cell is relaxed in a sweep only if
+// one of its points changed in its last relaxation or a neighbour cell changed a point on the
+// shared face since (an update is idempotent when no input changed, so the values, and the
+// sweep count, are still the FSM's).
+template <typename T, int R>
+__global__ void __launch_bounds__(CellCfg<R>::NT, MinBlocks<T, R>::value)
+k_dsweep(CellArgs A, int D)
+{
+    using C = CellCfg<R>;
+    constexpr int R3 = C::R3, NPL = C::NPL, NT = C::NT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CellSmem<T, R> Msm(smem_raw);
+    __shared__ CellShared<R> S;
+    const int tid = threadIdx.x;
+    Ctl* ctl = A.ctl;
+    const int cps = A.cps;
+    const uint32_t dir = ctl->sweep_idx & 7u;   // set by k_sweep_end (previous launch)
+    const uint32_t beg = A.diag_off[D], end = A.diag_off[D + 1];
+    T* Vt = reinterpret_cast<T*>(A.Vt);
+    const T* Ht = reinterpret_cast<const T*>(A.Ht);
+    uint32_t nupd = 0, nwr = 0, nsteps = 0;
+    unsigned long long nproc = 0, nw_cta = 0;
+    for (uint32_t w = beg + blockIdx.x; w < end; w += gridDim.x) {
+        const uint32_t e = A.diag_cells[w];
+        const int a = (int)(e % (uint32_t)cps), b = (int)((e / (uint32_t)cps) % (uint32_t)cps),
+                  cc = (int)(e / ((uint32_t)cps * (uint32_t)cps));
+        const int cx = (dir & 1u) ? cps - 1 - a : a, cy = (dir & 2u) ? cps - 1 - b : b,
+                  cz = (dir & 4u) ? cps - 1 - cc : cc;
+        const uint32_t c = (uint32_t)cx + (uint32_t)cps * ((uint32_t)cy + (uint32_t)cps * (uint32_t)cz);
+        EIK_CHECK(c < A.cap, "diagonal cell id");
+        __syncthreads();   // shared memory of the previous cell is free; S.cell consumed
+        if (tid == 0) {
+            S.cell = 1u;
+            if (A.locked) {
+                S.cell = A.cact[c];
+                A.cact[c] = 0;    // inputs consumed (re-set below or by a neighbour)
+            }
+            S.face_flag = 0;
+            S.stat[2] = 0;
+        }
+        __syncthreads();
+        if (!S.cell) continue;
+        ++nproc;
+        stage_cell_async<T, R>(Vt, Ht, Msm.V, Msm.H, c, cx, cy, cz, cps, A.cap);
+        __syncthreads();
+        const unsigned long long pm = (1ull << NPL) - 1ull;   // every plane, no gating (FSM)
+        switch (dir) {
+        case 0: sweep_dir<T, R, 0>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 1: sweep_dir<T, R, 1>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 2: sweep_dir<T, R, 2>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 3: sweep_dir<T, R, 3>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 4: sweep_dir<T, R, 4>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 5: sweep_dir<T, R, 5>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 6: sweep_dir<T, R, 6>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        default: sweep_dir<T, R, 7>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        }
+        // (sweep_dir ends with a barrier: every changed point carries the sign bit of hf)
+        unsigned long long nw = write_back_changed<T, R>(Vt + (int64_t)c * R3, Msm.V, Msm.H);
+        if (A.locked) {
+            // faces holding a changed point: the neighbour across them must run next time
+            uint32_t fm = 0;
+            for (int q = tid; q < 6 * R * R; q += NT) {
+                const int f = q / (R * R), uv = q - f * R * R, u = uv % R, v = uv / R;
+                int pa, pb, pd;
+                switch (f) {
+                case 0: pa = 0; pb = u; pd = v; break;
+                case 1: pa = R - 1; pb = u; pd = v; break;
+                case 2: pa = u; pb = 0; pd = v; break;
+                case 3: pa = u; pb = R - 1; pd = v; break;
+                case 4: pa = u; pb = v; pd = 0; break;
+                default: pa = u; pb = v; pd = R - 1; break;
+                }
+                if (Msm.H[pa + R * pb + R * R * pd] < T(0)) fm |= 1u << f;
+            }
+            for (int o = 16; o > 0; o >>= 1) fm |= __shfl_xor_sync(0xffffffffu, fm, o);
+            if ((tid & 31) == 0 && fm) atomicOr(&S.face_flag, fm);
+        }
+        for (int o = 16; o > 0; o >>= 1) nw += __shfl_xor_sync(0xffffffffu, nw, o);
+        if ((tid & 31) == 0 && nw) atomicAdd(&S.stat[2], nw);
+        __syncthreads();
+        if (tid == 0) nw_cta += S.stat[2];
+        if (A.locked) {
+            if (tid < 6 && (S.face_flag & (1u << tid))) {
+                const int64_t nc = face_neighbour(c, tid, cps);
+                if (nc >= 0) A.cact[nc] = 1;
+            }
+            if (tid == 6 && S.stat[2]) A.cact[c] = 1;   // its own points changed: run again
+        }
+    }
+    if (A.stats) {
+        unsigned long long u64 = nupd, w64 = nwr;
+        for (int o = 16; o > 0; o >>= 1) {
+            u64 += __shfl_xor_sync(0xffffffffu, u64, o);
+            w64 += __shfl_xor_sync(0xffffffffu, w64, o);
+        }
+        if ((tid & 31) == 0) {
+            if (u64) atomicAdd(&ctl->updates, u64);
+            if (w64) atomicAdd(&ctl->writes, w64);
+        }
+    }
+    if (tid == 0) {
+        if (nw_cta) atomicAdd(&ctl->sweep_writes, nw_cta);
+        if (nproc) {
+            atomicAdd(&ctl->processings, nproc);
+            atomicAdd(&ctl->sweeps, nproc);
+            atomicAdd(&ctl->bytes_written, nw_cta);
+        }
+    }
+    (void)R3;
 }
 
 // seed the async ring with the initial cells (L <- Q^c, Alg. 1 line 2)

@@ -19,7 +19,7 @@ def _declared():
 def test_header_declares_expected_api():
     names = _declared()
     for need in ("eik_create", "eik_solve", "eik_destroy", "eik_solve_host", "eik_get_stats",
-                 "eik_last_error"):
+                 "eik_last_error", "eik_solve_sweep"):
         assert need in names
 
 
@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(eik.lib, name), name
     assert set(_declared()) == set(eik.EXPORTS)
-    assert eik.lib.eik_abi_version() == 1
+    assert eik.lib.eik_abi_version() == 2
 
 
 def test_lib_is_sm100a_cubin():
@@ -41,8 +41,8 @@ def test_lib_is_sm100a_cubin():
 
 def test_stats_struct_layout_matches_header():
     import paper_1306_4743_b200 as eik
-    # 3*8 + 4*4 + 5*8 + 2*4 + 2*8 + 4*8 + 2*8 + 8 = 160 bytes
-    assert ctypes.sizeof(eik.EikStats) == 160
+    # 3*8 + 4*4 + 5*8 + 2*4 + 2*8 + 4*8 + 2*8 + 8 + 8 = 168 bytes
+    assert ctypes.sizeof(eik.EikStats) == 168
 
 
 def test_create_without_gpu_fails_cleanly():

@@ -66,8 +66,15 @@ typedef enum {
     EIK_OPT_MAX_SWEEPS = 6,  /* sweeps per cell processing before the cell saves its active
                                 points and re-queues itself (bounds the round length, which is
                                 the slowest cell's); 0 = until convergence [4]                   */
-    EIK_OPT_TIMEOUT_S = 7    /* device-side watchdog: the scheduler loop stops and the solve
+    EIK_OPT_TIMEOUT_S = 7,   /* device-side watchdog: the scheduler loop stops and the solve
                                 returns EIK_EINTERNAL after this many seconds [120]              */
+    EIK_OPT_KAPPA = 8        /* early termination threshold kappa >= 0 [0 = exact].
+                                eik_solve: a point change <= kappa activates no neighbour point
+                                and a border change <= kappa tags no neighbour cell (P:1192-
+                                1193).  eik_solve_sweep: stop after the first sweep whose
+                                largest change is <= kappa.  kappa > 0 returns an
+                                approximation of the discrete solution (values >= it; P:1187
+                                gives no error bound)                                            */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */

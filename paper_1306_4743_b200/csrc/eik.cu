@@ -34,6 +34,7 @@ struct eik_ctx {
     int time_cell_events = 0;
     int async_defer = 1;
     int max_sweeps = 4;
+    double kappa = 0.0;
     double timeout_s = 120.0;
     cudaEvent_t cev[2] = {nullptr, nullptr};
     double ms_cell_events = 0;
@@ -268,6 +269,10 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         if (value < 0 || value > 5) return fail(ctx, EIK_EINVAL, "defer mode must be 0..5");
         ctx->async_defer = (int)value;
         return EIK_OK;
+    case EIK_OPT_KAPPA:
+        if (!(value >= 0) || !isfinite(value)) return fail(ctx, EIK_EINVAL, "kappa must be finite and >= 0");
+        ctx->kappa = value;
+        return EIK_OK;
     case EIK_OPT_TIMEOUT_S:
         if (!(value > 0)) return fail(ctx, EIK_EINVAL, "timeout must be > 0 s");
         ctx->timeout_s = value;
@@ -458,8 +463,8 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
     // loop mode 2: rounds in a CUDA graph with a conditional WHILE node around one round
     char keybuf[256];
     // every value baked into the captured kernel parameters is part of the key
-    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d/%d", (int)sizeof(T), r, (long long)J,
-             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps, ca.fused);
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d/%d/%.17g", (int)sizeof(T), r, (long long)J,
+             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps, ca.fused, ca.kappa);
     if (!ctx->gexec || ctx->gkey != keybuf) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
         cudaGraph_t graph;
@@ -516,10 +521,14 @@ __global__ void k_sweep_end(Ctl* ctl, cudaGraphConditionalHandle h)
 {
     volatile Ctl* c = ctl;
     const unsigned long long w = c->sweep_writes;
+    const float dm = __uint_as_float(c->sweep_dmax);
     c->sweep_idx += 1;
     c->rounds += 1;
     c->sweep_writes = 0;
-    bool more = w != 0;
+    c->sweep_dmax = 0;
+    // stop after a sweep that changed nothing, or (kappa > 0) whose largest change was
+    // <= kappa
+    bool more = w != 0 && dm > c->kappa_f;
     if (more && c->sweep_idx >= c->max_rounds) { c->err |= 4u; more = false; }
     if (more && gtimer() - c->t_solve0 > c->budget_ns) { c->err |= 8u; more = false; }
     cudaGraphSetConditional(h, more ? 1u : 0u);
@@ -591,8 +600,8 @@ static int run_sweeps(eik_ctx* ctx, int r, int64_t J, CellArgs ca, int method)
                                                                : sweep_grid_r<T, 4>(ctx, &maxgrid);
     if (st) return st;
     char keybuf[256];
-    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%d/%d", (int)sizeof(T), r, (long long)J,
-             (long long)ca.n1, ca.Vt, ca.Ht, ca.stats, ca.locked);
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%d/%d/%.17g", (int)sizeof(T), r, (long long)J,
+             (long long)ca.n1, ca.Vt, ca.Ht, ca.stats, ca.locked, ca.kappa);
     if (!ctx->gexec_sw || ctx->gkey_sw != keybuf) {
         if (ctx->gexec_sw) { cudaGraphExecDestroy(ctx->gexec_sw); ctx->gexec_sw = nullptr; }
         cudaGraph_t graph;
@@ -648,6 +657,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     init.max_rounds = ctx->max_rounds;
     init.t_start = ~0ull;
     init.budget_ns = (unsigned long long)(ctx->timeout_s * 1e9);
+    init.kappa_f = (float)ctx->kappa;
     ctx->ms_cell_events = 0;
     *ctx->ctl_host = init;
     CK(cudaEventRecord(ctx->ev[0], s));
@@ -689,6 +699,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.cap = (uint32_t)J;
     ca.pend = ctx->pend;
     ca.pdir = ctx->pdir;
+    ca.kappa = ctx->kappa;
     ca.gen = ctx->gen;
     ca.n1 = n1;
     ca.cps = cps;

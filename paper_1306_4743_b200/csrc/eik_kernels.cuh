@@ -216,6 +216,8 @@ struct Ctl {
     // whole-grid sweeping (k_dsweep): sweep s runs direction s mod 8
     uint32_t sweep_idx;           // sweeps completed
     unsigned long long sweep_writes;   // strict decreases in the current sweep
+    uint32_t sweep_dmax;          // largest value change of the current sweep (float bits, up)
+    float kappa_f;                // early termination threshold of the sweeps
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -491,6 +493,12 @@ template <int R> struct CellCfg {
     static constexpr int LCAP = R == 16 ? 384 : (R == 8 ? 128 : 64);  // active-list capacity
 };
 
+#ifndef EIK_LIFO
+#define EIK_LIFO 1
+#endif
+#ifndef EIK_PARITY
+#define EIK_PARITY 1
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -534,6 +542,7 @@ struct CellArgs {
     const uint32_t* diag_off;        // [3 cps - 1]: start of each cell diagonal in diag_cells
     uint8_t* cact;                   // DLSM: cell has an input that changed since it last ran
     int32_t locked;                  // 1: DLSM (skip cells whose inputs did not change)
+    double kappa;                    // early termination threshold, >= 0
     int32_t fused;                   // round mode, bin width +inf: k_cell takes its cells straight
                                      // from the current worklist (the whole list is selected) and
                                      // its last CTA ends the round (no k_select / k_round_end)
@@ -600,7 +609,8 @@ template <typename T, int R, int DIR>
 __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& M,
                                               const uint16_t* __restrict__ ptab,
                                               unsigned long long pm, bool ungated,
-                                              uint32_t& nupd, uint32_t& nwr, uint32_t& nsteps)
+                                              uint32_t& nupd, uint32_t& nwr, uint32_t& nsteps,
+                                              T kap, T& dmax)
 {
     using C = CellCfg<R>;
     constexpr int R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL, NT = C::NT;
@@ -670,8 +680,11 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                         sts(qa, u);
                         if (hs > T(0)) sts(hb + up * TS, -hs);
                         ++nwr;
+                        // kappa: a change <= kappa activates nothing (ut = +inf)
+                        const T ut = (v - u > kap) ? u : INF;
+                        dmax = fmax(dmax, v - u);
                         const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
-                        const int bxa = (xb > u) & (ca > 0), bya = (yb > u) & (cb > 0), bza = (zb > u) & (cc > 0);
+                        const int bxa = (xb > ut) & (ca > 0), bya = (yb > ut) & (cb > 0), bza = (zb > ut) & (cc > 0);
                         sts_u8(bxa ? ab + up - oxp : scratch, 1u);
                         sts_u8(bya ? ab + up - oyp : scratch, 1u);
                         sts_u8(bza ? ab + up - ozp : scratch, 1u);
@@ -719,11 +732,13 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                         // lines 8-13: activate larger in-cell neighbours (the cross-border
                         // "currently downwind" test is done once per processing)
                         const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
+                        // kappa: a change <= kappa activates nothing (ut = +inf)
+                        const T ut = (v - u > kap) ? u : INF;
                         // activations as unconditional byte stores to either the neighbour
                         // or a scratch byte (short-lived compares, no predicate pressure)
-                        const int fxa = (xf > u) & (ca < R - 1), bxa = (xb > u) & (ca > 0);
-                        const int fya = (yf > u) & (cb < R - 1), bya = (yb > u) & (cb > 0);
-                        const int fza = (zf > u) & (cc < R - 1), bza = (zb > u) & (cc > 0);
+                        const int fxa = (xf > ut) & (ca < R - 1), bxa = (xb > ut) & (ca > 0);
+                        const int fya = (yf > ut) & (cb < R - 1), bya = (yb > ut) & (cb > 0);
+                        const int fza = (zf > ut) & (cc < R - 1), bza = (zb > ut) & (cc > 0);
                         sts_u8(fxa ? ab + up + oxp : scratch, 1u);
                         sts_u8(bxa ? ab + up - oxp : scratch, 1u);
                         sts_u8(fya ? ab + up + oyp : scratch, 1u);
@@ -880,6 +895,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     const int cx = (int)(c % (uint32_t)cps), cy = (int)((c / (uint32_t)cps) % (uint32_t)cps),
               cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
     const int64_t base = (int64_t)c * R3;
+    const T kap = (T)A.kappa;   // early termination threshold; 0 = exact
+    T dmax_ = T(0);             // (largest change: used by the whole-grid sweeps only)
     if (tid < 6) S.face_min[tid] = KEY_INF;
     if (tid == 0) {
         S.face_flag = 0;
@@ -1121,12 +1138,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                                     old = prev;
                                 }
                             };
-                            if (xm > u && i > 0) claim(p - 1);
-                            if (xp > u && i < R - 1) claim(p + 1);
-                            if (ym > u && j > 0) claim(p - R);
-                            if (yp > u && j < R - 1) claim(p + R);
-                            if (zm > u && k > 0) claim(p - R * R);
-                            if (zp > u && k < R - 1) claim(p + R * R);
+                            const T ut = (v - u > kap) ? u : INF;   // kappa: see sweep_dir
+                            if (xm > ut && i > 0) claim(p - 1);
+                            if (xp > ut && i < R - 1) claim(p + 1);
+                            if (ym > ut && j > 0) claim(p - R);
+                            if (yp > ut && j < R - 1) claim(p + R);
+                            if (zm > ut && k > 0) claim(p - R * R);
+                            if (zp > ut && k < R - 1) claim(p + R * R);
                         }
                     }
                 }
@@ -1235,14 +1253,14 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         {
             const bool ungated = first && nact >= R3 / 8;
             switch (dir) {
-            case 0: bwd = sweep_dir<T, R, 0>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            case 1: bwd = sweep_dir<T, R, 1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            case 2: bwd = sweep_dir<T, R, 2>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            case 3: bwd = sweep_dir<T, R, 3>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            case 4: bwd = sweep_dir<T, R, 4>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            case 5: bwd = sweep_dir<T, R, 5>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            case 6: bwd = sweep_dir<T, R, 6>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
-            default: bwd = sweep_dir<T, R, 7>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps); break;
+            case 0: bwd = sweep_dir<T, R, 0>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            case 1: bwd = sweep_dir<T, R, 1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            case 2: bwd = sweep_dir<T, R, 2>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            case 3: bwd = sweep_dir<T, R, 3>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            case 4: bwd = sweep_dir<T, R, 4>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            case 5: bwd = sweep_dir<T, R, 5>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            case 6: bwd = sweep_dir<T, R, 6>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
+            default: bwd = sweep_dir<T, R, 7>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
             }
         }
         if (tid == 0) S.tm[5] += clock64() - tm1;
@@ -1279,7 +1297,10 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             if (sH[pp] < T(0)) {
                 const T val = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
                 const T out = sV[(ha + 1) + RP * (hb + 1) + RP2 * (hd + 1)];
-                if (val < out) fm = min(fm, key_bits(val));
+                // kappa: a border change <= kappa tags no neighbour cell (the tile in
+                // global memory still holds the value staged at the start of the processing)
+                const bool sig = kap == T(0) || __ldcg(&Vt[base + pp]) - val > kap;
+                if (val < out && sig) fm = min(fm, key_bits(val));
             }
         }
         if (f_prev >= 0 && fm != KEY_INF) { atomicMin(&S.face_min[f_prev], fm); atomicOr(&S.face_flag, 1u << f_prev); }
@@ -1368,6 +1389,14 @@ k_cell(CellArgs A)
     const uint32_t nproc = A.fused ? ctl->wl_count[cur] : ctl->proc_count;
     const uint32_t* wl = cur ? A.wl1 : A.wl0;
     uint32_t* wn = nx ? A.wl1 : A.wl0;
+    // Fused rounds keep the state bits of the two rounds apart (byte 0 / byte 2 by round
+    // parity): a cell takes this round's bits when claimed, and a tag during the round always
+    // goes to the next round's byte -- as with k_select, which takes every selected cell's
+    // bits before the round starts.  (Merging a tag into a not-yet-claimed cell of this round
+    // instead lets it run with faces that are only partly final: measured 13-25 % more
+    // processings on the paper's r = 8 suite.)
+    const uint32_t sh_cur = (A.fused && EIK_PARITY) ? 16u * (ctl->rounds & 1u) : 0u;
+    const uint32_t sh_nx = (A.fused && EIK_PARITY) ? 16u - sh_cur : 0u;
     // dynamic claiming of this round's cells (processing times vary by >10x between cells)
     bool worked = false;
     for (;;) {
@@ -1378,9 +1407,10 @@ k_cell(CellArgs A)
                 if (A.fused) {
                     // LIFO: the cells appended last (re-activated by the previous round's
                     // slowest processings: the critical path) are claimed first
-                    const uint32_t wi = nproc - 1u - w;
+                    const uint32_t wi = EIK_LIFO ? nproc - 1u - w : w;
                     cc = wl[wi];
-                    fl = atomicExch(&A.state[cc], 0u);   // take the inflow bits; leaves the list
+                    // take this round's inflow bits; the cell leaves the list
+                    fl = (atomicAnd(&A.state[cc], ~(0xffu << sh_cur)) >> sh_cur) & 0xffu;
                     A.key[cc] = KEY_INF;                 // V^c <- +inf on removal
                     atomicAdd(&ctl->proc_count, 1u);
                 } else {
@@ -1410,8 +1440,8 @@ k_cell(CellArgs A)
             if (nc >= 0) {
                 const uint32_t kb = S.face_min[tid];
                 atomicMin(&A.key[nc], kb);                                     // Eq. (3)
-                const uint32_t old = atomicOr(&A.state[nc], 1u << (tid ^ 1));  // face of nc
-                if (old == 0u) {                                               // Alg. 5
+                const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) << sh_nx);  // face of nc
+                if (((old >> sh_nx) & 0xffu) == 0u) {                                   // Alg. 5
                     const uint32_t sl = atomicAdd(&ctl->wl_count[nx], 1u);
                     wn[sl] = (uint32_t)nc;
                 }
@@ -1420,8 +1450,8 @@ k_cell(CellArgs A)
         }
         if (tid == 0 && S.cont) {   // continue this cell in a later round
             atomicMin(&A.key[c], S.cont_key);
-            const uint32_t old = atomicOr(&A.state[c], FLAG_CONT);
-            if (old == 0u) {
+            const uint32_t old = atomicOr(&A.state[c], FLAG_CONT << sh_nx);
+            if (((old >> sh_nx) & 0xffu) == 0u) {
                 const uint32_t sl = atomicAdd(&ctl->wl_count[nx], 1u);
                 wn[sl] = c;
             }
@@ -1598,6 +1628,10 @@ k_async(CellArgs A)
     if (tid == 0) atomicMax(&ctl->t_end, gtimer());
 }
 
+// a change as a float rounded up (non-negative: its bits order like the values)
+__device__ __forceinline__ float dmax_up(float x) { return x; }
+__device__ __forceinline__ float dmax_up(double x) { return __double2float_ru(x); }
+
 // --------------------------------------------------------------------------------------
 // Whole-grid sweeping: the paper's comparison methods on the same tiles.
 // FSM relaxes every gridpoint once per sweep in one of the 2^3 loop orderings;
@@ -1632,6 +1666,8 @@ k_dsweep(CellArgs A, int D)
     const T* Ht = reinterpret_cast<const T*>(A.Ht);
     uint32_t nupd = 0, nwr = 0, nsteps = 0;
     unsigned long long nproc = 0, nw_cta = 0;
+    const T kap = (T)A.kappa;
+    T dmax = T(0);   // largest change of this thread (the sweep stops once it is <= kappa)
     for (uint32_t w = beg + blockIdx.x; w < end; w += gridDim.x) {
         const uint32_t e = A.diag_cells[w];
         const int a = (int)(e % (uint32_t)cps), b = (int)((e / (uint32_t)cps) % (uint32_t)cps),
@@ -1657,14 +1693,14 @@ k_dsweep(CellArgs A, int D)
         __syncthreads();
         const unsigned long long pm = (1ull << NPL) - 1ull;   // every plane, no gating (FSM)
         switch (dir) {
-        case 0: sweep_dir<T, R, 0>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        case 1: sweep_dir<T, R, 1>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        case 2: sweep_dir<T, R, 2>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        case 3: sweep_dir<T, R, 3>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        case 4: sweep_dir<T, R, 4>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        case 5: sweep_dir<T, R, 5>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        case 6: sweep_dir<T, R, 6>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
-        default: sweep_dir<T, R, 7>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps); break;
+        case 0: sweep_dir<T, R, 0>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        case 1: sweep_dir<T, R, 1>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        case 2: sweep_dir<T, R, 2>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        case 3: sweep_dir<T, R, 3>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        case 4: sweep_dir<T, R, 4>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        case 5: sweep_dir<T, R, 5>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        case 6: sweep_dir<T, R, 6>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
+        default: sweep_dir<T, R, 7>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
         }
         // (sweep_dir ends with a barrier: every changed point carries the sign bit of hf)
         unsigned long long nw = write_back_changed<T, R>(Vt + (int64_t)c * R3, Msm.V, Msm.H);
@@ -1709,6 +1745,11 @@ k_dsweep(CellArgs A, int D)
             if (u64) atomicAdd(&ctl->updates, u64);
             if (w64) atomicAdd(&ctl->writes, w64);
         }
+    }
+    {
+        float dm = dmax_up(dmax);
+        for (int o = 16; o > 0; o >>= 1) dm = fmaxf(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+        if ((tid & 31) == 0 && dm > 0.f) atomicMax(&ctl->sweep_dmax, __float_as_uint(dm));
     }
     if (tid == 0) {
         if (nw_cta) atomicAdd(&ctl->sweep_writes, nw_cta);

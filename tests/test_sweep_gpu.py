@@ -117,3 +117,32 @@ def test_hcm_after_sweep_same_ctx(solver):
         U2 = solver.solve(torch.from_numpy(F).cuda(), torch.from_numpy(m).cuda(),
                           torch.from_numpy(q).cuda(), cell_size=8, n=w.n).cpu().numpy()
         _check(U2.reshape(w.F.shape), U_orc, w, np.float64)
+
+
+# ---- kappa early termination: not a parity claim (the paper
+# gives no error bound) -- what holds: kappa = 0 is the exact path, values stay upper
+# bounds of the discrete solution (monotone scheme: every value ever held is >= it), the
+# finite/infinite mask is unchanged, and a sweep method stops no later
+@pytest.mark.parametrize("case", ["ex3", "rand", "c3"])
+def test_kappa_early_termination(solver, case):
+    import paper_1306_4743_b200 as eik
+    import torch
+    w = dict(CASES)[case]()
+    U_orc = oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals, h=w.h)
+    fin = np.isfinite(U_orc)
+    F, m, q = (torch.from_numpy(a).cuda() for a in w.as_dtype(np.float64))
+    res = {}
+    for kap in (0.0, 1e-8, 1e-4):
+        solver.set_option(eik.EIK_OPT_KAPPA, kap)
+        try:
+            U = solver.solve(F, m, q, cell_size=8, n=w.n, h=w.h).cpu().numpy().reshape(w.F.shape)
+            Us, st = _sweep(solver, w, np.float64, 8, "dlsm")
+        finally:
+            solver.set_option(eik.EIK_OPT_KAPPA, 0.0)
+        for V in (U, Us):
+            assert np.array_equal(np.isfinite(V), fin)
+            assert (V[fin] >= U_orc[fin] - 1e-12).all()
+        res[kap] = (U, Us, st["grid_sweeps"])
+    _check(res[0.0][0], U_orc, w, np.float64)
+    _check(res[0.0][1], U_orc, w, np.float64)
+    assert res[1e-4][2] <= res[1e-8][2] <= res[0.0][2]

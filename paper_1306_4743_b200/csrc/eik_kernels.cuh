@@ -496,6 +496,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_LIFO
 #define EIK_LIFO 1
 #endif
+#ifndef EIK_DIR_TEMPLATE_MIN_R
+#define EIK_DIR_TEMPLATE_MIN_R 16   // cells below this size use the runtime-direction sweep
+#endif
 #ifndef EIK_PARITY
 #define EIK_PARITY 1
 #endif
@@ -602,20 +605,25 @@ template <typename T, int R> struct CellSmem {
     }
 };
 
-// One wavefront sweep in the compile-time direction DIR (bit0/1/2 = x/y/z descending): the
-// direction's reflection mask and neighbour offsets are immediates.  Returns the axes along
-// which points behind the wavefront were activated (bit0 x, bit1 y, bit2 z).
+// One wavefront sweep in direction DIR (bit0/1/2 = x/y/z descending).  DIR >= 0: a
+// compile-time direction, whose reflection mask and neighbour offsets are immediates (one
+// instantiation per direction: r = 16, where a step is long enough to pay for the code
+// size); DIR = -1: the direction is the runtime argument rdir (one instantiation: r <= 8,
+// where eight copies of the sweep overflow the instruction cache -- measured 3.3x slower on
+// the paper's r = 8 fp64 suite).  Returns the axes along which points behind the wavefront
+// were activated (bit0 x, bit1 y, bit2 z).
 template <typename T, int R, int DIR>
 __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& M,
                                               const uint16_t* __restrict__ ptab,
                                               unsigned long long pm, bool ungated,
                                               uint32_t& nupd, uint32_t& nwr, uint32_t& nsteps,
-                                              T kap, T& dmax)
+                                              T kap, T& dmax, int rdir = 0)
 {
     using C = CellCfg<R>;
     constexpr int R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL, NT = C::NT;
     constexpr int TS = (int)sizeof(T);
-    constexpr bool fx = DIR & 1, fy = DIR & 2, fz = DIR & 4;
+    const int dv = DIR >= 0 ? DIR : rdir;
+    const bool fx = dv & 1, fy = dv & 2, fz = dv & 4;
     const int tid = threadIdx.x;
     const T INF = dinf<T>();
     // shared-window bases: V box (at the first interior point), hf, activity bytes
@@ -631,12 +639,12 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     // XORs its field); in canonical coordinates "forward" along an axis is +1 and the
     // forward / backward neighbours exist iff the coordinate is < R-1 / > 0.  Box and flag
     // offsets (bytes) of the forward neighbours are compile-time constants.
-    constexpr unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
+    const unsigned dm = (fx ? R - 1 : 0) | (fy ? (R - 1) * R : 0) | (fz ? (R - 1) * R * R : 0);
     // (unsigned: address arithmetic wraps modulo 2^32, a negative offset subtracts)
-    constexpr uint32_t oxq = (uint32_t)((fx ? -1 : 1) * TS), oyq = (uint32_t)((fy ? -RP : RP) * TS),
-                       ozq = (uint32_t)((fz ? -RP2 : RP2) * TS);
-    constexpr uint32_t oxp = (uint32_t)(fx ? -1 : 1), oyp = (uint32_t)(fy ? -R : R),
-                       ozp = (uint32_t)(fz ? -R * R : R * R);
+    const uint32_t oxq = (uint32_t)((fx ? -1 : 1) * TS), oyq = (uint32_t)((fy ? -RP : RP) * TS),
+                   ozq = (uint32_t)((fz ? -RP2 : RP2) * TS);
+    const uint32_t oxp = (uint32_t)(fx ? -1 : 1), oyp = (uint32_t)(fy ? -R : R),
+                   ozp = (uint32_t)(fz ? -R * R : R * R);
     // Two-stage prefetch, independent of the current step's results: at step s the thread
     // holds its entry en / hf hn of plane s and the entry en1 of plane s + 1; the step loads
     // hf of plane s + 1 (shared memory) and the entry of plane s + 2 (global table via L1),
@@ -1252,7 +1260,9 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         uint32_t bwd = 0;
         {
             const bool ungated = first && nact >= R3 / 8;
-            switch (dir) {
+            if constexpr (R < EIK_DIR_TEMPLATE_MIN_R) {
+                bwd = sweep_dir<T, R, -1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_, dir);
+            } else switch (dir) {
             case 0: bwd = sweep_dir<T, R, 0>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
             case 1: bwd = sweep_dir<T, R, 1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
             case 2: bwd = sweep_dir<T, R, 2>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
@@ -1692,7 +1702,9 @@ k_dsweep(CellArgs A, int D)
         stage_cell_async<T, R>(Vt, Ht, Msm.V, Msm.H, c, cx, cy, cz, cps, A.cap);
         __syncthreads();
         const unsigned long long pm = (1ull << NPL) - 1ull;   // every plane, no gating (FSM)
-        switch (dir) {
+        if constexpr (R < EIK_DIR_TEMPLATE_MIN_R) {
+            sweep_dir<T, R, -1>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax, (int)dir);
+        } else switch (dir) {
         case 0: sweep_dir<T, R, 0>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
         case 1: sweep_dir<T, R, 1>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
         case 2: sweep_dir<T, R, 2>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;

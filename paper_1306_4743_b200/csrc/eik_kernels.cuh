@@ -1393,6 +1393,8 @@ k_cell(CellArgs A)
     __shared__ CellShared<R> S;
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
+    // graph body with several rounds: the rounds after the last one are no-ops
+    if (A.graph && ctl->done) return;
     const uint32_t cur = ctl->cur, nx = cur ^ 1u;
     // fused: this round's cells are the whole current worklist (Alg. 1 lines 4-5 with an
     // infinite bin); otherwise k_select built the proc list

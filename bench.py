@@ -346,7 +346,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
             "config": dict(config_block(cfg, prec, r, n), **({"solve": f"eik_solve_sweep ({args.method}): "
-                           "ingest + whole-grid sweep loop (CUDA graph) + egress"} if sweep else {})),
+                           "ingest + whole-grid sweep loop (CUDA graph) + egress"} if sweep else {}),
+                           **({"bin_width": args.bin_width} if args.bin_width is not None else {})),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             # per solve: init, ingest, (worklist build), egress + the loop's launches: fused
             # rounds = one k_cell each (k_select + k_cell + k_round_end otherwise); sweeping =

@@ -395,6 +395,7 @@ static int enqueue_round(eik_ctx* ctx, int r, const CellArgs& ca, int sel_grid, 
 
 __global__ void k_round_end_graph(Ctl* ctl, cudaGraphConditionalHandle h)
 {
+    if (ctl->done) return;   // the solve ended in an earlier round of this iteration
     cudaGraphSetConditional(h, round_end_body(ctl) ? 0u : 1u);
 }
 
@@ -498,8 +499,12 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
             // several rounds per WHILE iteration: plain kernel-to-kernel edges between them
             for (int k = 0; k < EIK_ROUNDS_PER_ITER && !st; ++k) st = enqueue_round<T>(ctx, r, cg, sg, cgrid);
         } else {
-            st = enqueue_round<T>(ctx, r, ca, sg, cgrid);
-            k_round_end_graph<<<1, 1, 0, cs>>>(ctx->ctl, handle);
+            CellArgs cg = ca;
+            cg.graph = 1;   // (non-fused: only turns the rounds after the last into no-ops)
+            for (int k = 0; k < EIK_ROUNDS_PER_ITER && !st; ++k) {
+                st = enqueue_round<T>(ctx, r, cg, sg, cgrid);
+                k_round_end_graph<<<1, 1, 0, cs>>>(ctx->ctl, handle);
+            }
         }
         cudaGraph_t captured;
         cudaError_t ce = cudaStreamEndCapture(cs, &captured);

@@ -397,6 +397,7 @@ __global__ void k_build_wl(const uint32_t* __restrict__ key, const uint32_t* __r
 __global__ void k_select(Ctl* ctl, uint32_t* wl0, uint32_t* wl1, uint32_t* proc_cell,
                          uint32_t* proc_flags, uint32_t* key, uint32_t* state, float delta)
 {
+    if (ctl->done) return;   // a round after the last one in the same graph iteration
     const uint32_t cur = ctl->cur, nx = cur ^ 1u;
     const uint32_t n = ctl->wl_count[cur];
     const uint32_t* wl = cur ? wl1 : wl0;

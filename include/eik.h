@@ -68,13 +68,18 @@ typedef enum {
                                 the slowest cell's); 0 = until convergence [4]                   */
     EIK_OPT_TIMEOUT_S = 7,   /* device-side watchdog: the scheduler loop stops and the solve
                                 returns EIK_EINTERNAL after this many seconds [120]              */
-    EIK_OPT_KAPPA = 8        /* early termination threshold kappa >= 0 [0 = exact].
+    EIK_OPT_KAPPA = 8,       /* early termination threshold kappa >= 0 [0 = exact].
                                 eik_solve: a point change <= kappa activates no neighbour point
                                 and a border change <= kappa tags no neighbour cell (P:1192-
                                 1193).  eik_solve_sweep: stop after the first sweep whose
                                 largest change is <= kappa.  kappa > 0 returns an
                                 approximation of the discrete solution (values >= it; P:1187
                                 gives no error bound)                                            */
+    EIK_OPT_CELL_KEY = 9     /* cell value of a tag (Alg. 1 line 9): 0 = Eq. (3), the smallest
+                                newly updated inflow value, reset to +inf on removal [0];
+                                1 = the legacy Eq. (4): V_max + D / F(y), never
+                                reset.  Orders work only (bin width < inf, async readiness);
+                                the fixed point is the same                          */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */

@@ -39,6 +39,7 @@ struct eik_ctx {
     int async_defer = 1;
     int max_sweeps = 4;
     double kappa = 0.0;
+    int legacy_key = 0;
     double timeout_s = 120.0;
     cudaEvent_t cev[2] = {nullptr, nullptr};
     double ms_cell_events = 0;
@@ -277,6 +278,10 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         if (!(value >= 0) || !isfinite(value)) return fail(ctx, EIK_EINVAL, "kappa must be finite and >= 0");
         ctx->kappa = value;
         return EIK_OK;
+    case EIK_OPT_CELL_KEY:
+        if (value != 0 && value != 1) return fail(ctx, EIK_EINVAL, "cell key must be 0 (Eq. 3) or 1 (Eq. 4)");
+        ctx->legacy_key = (int)value;
+        return EIK_OK;
     case EIK_OPT_TIMEOUT_S:
         if (!(value > 0)) return fail(ctx, EIK_EINVAL, "timeout must be > 0 s");
         ctx->timeout_s = value;
@@ -380,7 +385,7 @@ static int enqueue_round(eik_ctx* ctx, int r, const CellArgs& ca, int sel_grid, 
     if (!ca.fused) {   // fused: k_cell selects the whole worklist itself
         k_select<<<sel_grid, 256, 0, ctx->stream>>>(ctx->ctl, ctx->wl0, ctx->wl1, ctx->proc_cell,
                                                      ctx->proc_flags, ctx->key, ctx->state,
-                                                     (float)ctx->bin_width);
+                                                     (float)ctx->bin_width, ca.legacy_key);
         CK(cudaGetLastError());
     }
     if (time_events) CK(cudaEventRecord(ctx->cev[0], ctx->stream));
@@ -468,8 +473,8 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
     // loop mode 2: rounds in a CUDA graph with a conditional WHILE node around one round
     char keybuf[256];
     // every value baked into the captured kernel parameters is part of the key
-    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d/%d/%.17g", (int)sizeof(T), r, (long long)J,
-             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps, ca.fused, ca.kappa);
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d/%d/%.17g/%d", (int)sizeof(T), r, (long long)J,
+             (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps, ca.fused, ca.kappa, ca.legacy_key);
     if (!ctx->gexec || ctx->gkey != keybuf) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }
         cudaGraph_t graph;
@@ -710,6 +715,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.pend = ctx->pend;
     ca.pdir = ctx->pdir;
     ca.kappa = ctx->kappa;
+    ca.legacy_key = ctx->legacy_key;
     ca.gen = ctx->gen;
     ca.n1 = n1;
     ca.cps = cps;

@@ -395,7 +395,8 @@ __global__ void k_build_wl(const uint32_t* __restrict__ key, const uint32_t* __r
 // A7: select the lowest bin [kmin, kmin + delta] of the current worklist
 // --------------------------------------------------------------------------------------
 __global__ void k_select(Ctl* ctl, uint32_t* wl0, uint32_t* wl1, uint32_t* proc_cell,
-                         uint32_t* proc_flags, uint32_t* key, uint32_t* state, float delta)
+                         uint32_t* proc_flags, uint32_t* key, uint32_t* state, float delta,
+                         int legacy_key)
 {
     if (ctl->done) return;   // a round after the last one in the same graph iteration
     const uint32_t cur = ctl->cur, nx = cur ^ 1u;
@@ -413,7 +414,7 @@ __global__ void k_select(Ctl* ctl, uint32_t* wl0, uint32_t* wl1, uint32_t* proc_
         uint32_t fl = 0;
         if (sel) {
             fl = atomicExch(&state[c], 0u);   // take the inflow bits; cell leaves the list
-            key[c] = KEY_INF;                 // V^c <- +inf on removal
+            if (!legacy_key) key[c] = KEY_INF;   // V^c <- +inf on removal (not Eq. (4))
         }
         // selected -> proc list (cell, flags): same slot for both arrays
         {
@@ -547,6 +548,7 @@ struct CellArgs {
     uint8_t* cact;                   // DLSM: cell has an input that changed since it last ran
     int32_t locked;                  // 1: DLSM (skip cells whose inputs did not change)
     double kappa;                    // early termination threshold, >= 0
+    int32_t legacy_key;              // 1: cell value of Eq. (4), no reset on removal
     int32_t fused;                   // round mode, bin width +inf: k_cell takes its cells straight
                                      // from the current worklist (the whole list is selected) and
                                      // its last CTA ends the round (no k_select / k_round_end)
@@ -577,6 +579,7 @@ template <> struct Vec16<double> { using type = double2; };
 template <int R> struct CellShared {
     unsigned long long plane[2];
     uint32_t face_min[6];              // Eq. (3) min newly-updated inflow value per face
+    uint32_t face_max[6];              // Eq. (4) max newly-updated inflow value per face
     uint32_t face_flag;                // faces whose neighbour is currently downwind
     unsigned long long stat[3];
     uint32_t cell, flags;              // async mode broadcast
@@ -906,7 +909,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     const int64_t base = (int64_t)c * R3;
     const T kap = (T)A.kappa;   // early termination threshold; 0 = exact
     T dmax_ = T(0);             // (largest change: used by the whole-grid sweeps only)
-    if (tid < 6) S.face_min[tid] = KEY_INF;
+    if (tid < 6) { S.face_min[tid] = KEY_INF; S.face_max[tid] = 0u; }
     if (tid == 0) {
         S.face_flag = 0;
         S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
@@ -1286,7 +1289,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // halo value, an upper bound of the current one: P:718 redundant tags are harmless); the
     // cell key candidate is the smallest such value (A_new of Eq. (3)).
     {
-        uint32_t fm = KEY_INF;
+        uint32_t fm = KEY_INF, fx = 0u;
         int f_prev = -1;
         for (int e = tid; e < 6 * R * R; e += NT) {
             const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
@@ -1300,8 +1303,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             default: a = u; b = v; d = R - 1; ha = a; hb = b; hd = R; break;
             }
             if (f != f_prev) {
-                if (f_prev >= 0 && fm != KEY_INF) { atomicMin(&S.face_min[f_prev], fm); atomicOr(&S.face_flag, 1u << f_prev); }
+                if (f_prev >= 0 && fm != KEY_INF) {
+                    atomicMin(&S.face_min[f_prev], fm);
+                    atomicOr(&S.face_flag, 1u << f_prev);
+                    if (A.legacy_key) atomicMax(&S.face_max[f_prev], fx);
+                }
                 fm = KEY_INF;
+                fx = 0u;
                 f_prev = f;
             }
             const int pp = a + R * b + R * R * d;
@@ -1311,10 +1319,17 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 // kappa: a border change <= kappa tags no neighbour cell (the tile in
                 // global memory still holds the value staged at the start of the processing)
                 const bool sig = kap == T(0) || __ldcg(&Vt[base + pp]) - val > kap;
-                if (val < out && sig) fm = min(fm, key_bits(val));
+                if (val < out && sig) {
+                    fm = min(fm, key_bits(val));
+                    fx = max(fx, key_bits(val));
+                }
             }
         }
-        if (f_prev >= 0 && fm != KEY_INF) { atomicMin(&S.face_min[f_prev], fm); atomicOr(&S.face_flag, 1u << f_prev); }
+        if (f_prev >= 0 && fm != KEY_INF) {
+            atomicMin(&S.face_min[f_prev], fm);
+            atomicOr(&S.face_flag, 1u << f_prev);
+            if (A.legacy_key) atomicMax(&S.face_max[f_prev], fx);
+        }
     }
     __syncthreads();
 
@@ -1346,6 +1361,21 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         S.nsteps = nsteps;
         atomicAdd(&A.ctl->dbg[40], (unsigned long long)S.tm[6]);
     }
+}
+
+// Cell value a tag from face f proposes for the neighbour cell nc (Alg. 1 line 9):
+//   Eq. (3) (default): the smallest newly updated inflow value of the face;
+//   Eq. (4) (legacy): V_max + D / F(y), V_max the largest newly updated inflow
+//   value, D = (h^c + h) / 2 the distance from the face's gridpoints to the centre of nc and
+//   F(y) the speed there (the gridpoint (r/2, r/2, r/2) of nc): D / F(y) = (r + 1) / 2 * hf.
+template <typename T, int R>
+__device__ __forceinline__ uint32_t tag_key(const CellArgs& A, const CellShared<R>& S, int f, int64_t nc)
+{
+    if (!A.legacy_key) return S.face_min[f];
+    const T hfc = __ldcg(reinterpret_cast<const T*>(A.Ht) + nc * (int64_t)(R * R * R) +
+                         (R / 2) * (1 + R + R * R));
+    const float v = __uint_as_float(S.face_max[f]) + (float)(T(0.5 * (R + 1)) * hfc);
+    return key_bits(v);
 }
 
 // neighbour cell across face f of c, or -1 outside the grid
@@ -1424,7 +1454,7 @@ k_cell(CellArgs A)
                     cc = wl[wi];
                     // take this round's inflow bits; the cell leaves the list
                     fl = (atomicAnd(&A.state[cc], ~(0xffu << sh_cur)) >> sh_cur) & 0xffu;
-                    A.key[cc] = KEY_INF;                 // V^c <- +inf on removal
+                    if (!A.legacy_key) A.key[cc] = KEY_INF;   // V^c <- +inf on removal
                     atomicAdd(&ctl->proc_count, 1u);
                 } else {
                     cc = A.proc_cell[w];
@@ -1451,8 +1481,8 @@ k_cell(CellArgs A)
         if (tid < 6 && (S.face_flag & (1u << tid))) {
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
-                const uint32_t kb = S.face_min[tid];
-                atomicMin(&A.key[nc], kb);                                     // Eq. (3)
+                const uint32_t kb = tag_key<T, R>(A, S, tid, nc);
+                atomicMin(&A.key[nc], kb);                                     // Eq. (3) / (4)
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) << sh_nx);  // face of nc
                 if (((old >> sh_nx) & 0xffu) == 0u) {                                   // Alg. 5
                     const uint32_t sl = atomicAdd(&ctl->wl_count[nx], 1u);
@@ -1589,7 +1619,7 @@ k_async(CellArgs A)
             }
             if (got != Q_EMPTY) {
                 fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
-                A.key[got] = KEY_INF;                                // V^c <- +inf
+                if (!A.legacy_key) A.key[got] = KEY_INF;             // V^c <- +inf
                 __threadfence();
             }
             S.cell = got;
@@ -1611,7 +1641,7 @@ k_async(CellArgs A)
         if (tid < 6 && (S.face_flag & (1u << tid))) {
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
-                atomicMin(&A.key[nc], S.face_min[tid]);                       // Eq. (3)
+                atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
                 if (A.defer == 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
                 if (!(old & (ST_QUEUED | ST_RUNNING))) q_push(ctl, ring, A.qmask, (uint32_t)nc);

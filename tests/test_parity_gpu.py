@@ -262,3 +262,19 @@ def test_solve_on_a_side_stream():
     st.synchronize()
     assert_parity(U.cpu().numpy(), oracle_U(w), w, np.float32)
     s.close()
+
+
+@pytest.mark.parametrize("mode,delta,defer", [(2, 0.02, 1), (2, 0.0, 1), (1, 0.05, 1), (0, 0.0, 2),
+                                               (2, float("inf"), 1)])
+def test_legacy_cell_key_same_fixed_point(mode, delta, defer):
+    """Eq. (4)'s legacy cell value (no reset on removal) only
+    reorders work: the fixed point is the same."""
+    import paper_1306_4743_b200 as eik
+    s = eik.Solver(device=0, loop_mode=mode, bin_width=delta)
+    s.set_option(eik.EIK_OPT_CELL_KEY, 1)
+    s.set_option(eik.EIK_OPT_ASYNC_DEFER, defer)
+    for w in (W.c3(48), W.c4(48), W.paper_shell_maze(24)):
+        for r in (8, 16):
+            for dt in (np.float64, np.float32):
+                assert_parity(_gpu(s, w, dt, r), oracle_U(w), w, dt)
+    s.close()

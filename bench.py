@@ -216,6 +216,10 @@ def config_block(cfg, prec, r, n=None):
             if n >= 256 else "L2-resident (small config)"}
 
 
+def sweep_method(args):
+    return getattr(args, "method", "hcm") != "hcm"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -227,7 +231,10 @@ def main():
     ap.add_argument("--ref-n", type=int, default=128, help="oracle sample size for --impl reference")
     ap.add_argument("--cpu-n", type=int, default=256, help="oracle sample size for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--bin-width", type=float, default=None)
+    ap.add_argument("--bin-width", type=float, default=None,
+                    help="priority bin width (round modes; implies --loop-mode 2)")
+    ap.add_argument("--loop-mode", type=int, default=None,
+                    help="scheduler (EIK_OPT_LOOP_MODE): 0 async [library default], 1 host rounds, 2 graph rounds")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--method", default="hcm", choices=["hcm", "dfsm", "dlsm"],
                     help="hcm: the product path (eik_solve); dfsm / dlsm: the paper's comparison "
@@ -257,7 +264,9 @@ def main():
     n, F, m, q = make_inputs(cfg, prec, dev, args.n)
     M = (n + 1) ** 3
     s_bytes = 4 if prec == "f32" else 8
-    solver = eik.Solver(device=local, bin_width=args.bin_width)
+    loop_mode = args.loop_mode if args.loop_mode is not None else (2 if args.bin_width is not None else None)
+    solver = eik.Solver(device=local, bin_width=args.bin_width, loop_mode=loop_mode)
+    async_mode = loop_mode in (None, 0) and not sweep_method(args)
     U = torch.empty_like(F)
     stream = torch.cuda.current_stream(dev)
 
@@ -295,7 +304,9 @@ def main():
     # event-timed cross-check of the same kernel (host-loop mode, CUDA events around launches)
     st2 = {"ms_cell_events": 0.0, "cell_launches": 1}
     if not sweep:
-        s2 = eik.Solver(device=local, loop_mode=1, bin_width=args.bin_width)
+        # CUDA events around every cell-kernel launch: the persistent k_async launch in async
+        # mode, else every round's launch in the host-driven loop
+        s2 = eik.Solver(device=local, loop_mode=0 if async_mode else 1, bin_width=args.bin_width)
         s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
         s2.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=torch.empty_like(F))
         st2 = s2.stats()
@@ -308,7 +319,7 @@ def main():
     st = stats[-1]
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": f"{'k_dsweep' if sweep else 'k_cell'}<{'float' if prec == 'f32' else 'double'},{r}>",
+            "kernel": f"{'k_dsweep' if sweep else 'k_async' if async_mode else 'k_cell'}<{'float' if prec == 'f32' else 'double'},{r}>",
             "alg_bytes_per_launch": alg_bytes / max(launches, 1),
             "ms_per_launch_device": cell_ms / max(launches, 1),
             "ms_per_launch_events": (st2["ms_cell_events"] / max(st2["cell_launches"], 1)),
@@ -352,7 +363,9 @@ def main():
             # per solve: init, ingest, (worklist build), egress + the loop's launches: fused
             # rounds = one k_cell each (k_select + k_cell + k_round_end otherwise); sweeping =
             # one k_dsweep per cell diagonal + k_sweep_end per sweep
-            "gpu_launches": int(args.steps * (4 + (launches + rounds if sweep else
+            # async: init, ingest, seed, the persistent k_async, egress
+            "gpu_launches": int(args.steps * (5 if async_mode else
+                                              4 + (launches + rounds if sweep else
                                                    rounds * (1 if args.bin_width is None else 3)))),
             "clocks": clk.summary(),
             "method": args.method,

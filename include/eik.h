@@ -53,19 +53,27 @@ typedef enum {
     EIK_OPT_MAX_ROUNDS = 1,  /* safety cap on scheduler rounds; exceeding it = EIK_EINTERNAL
                                 [1e9]                                                           */
     EIK_OPT_LOOP_MODE = 2,   /* 0 = asynchronous persistent kernel (CTAs pull cells from a
-                                device ring; no rounds, no host round-trip);
+                                device ring with ticket pops; no rounds, no host round-trip)
+                                [default];
                                 1 = bulk-synchronous rounds driven by the host (debug);
                                 2 = bulk-synchronous rounds in a CUDA graph WHILE node, no host
-                                round-trip per round [default]                                   */
+                                round-trip per round.  The bin width applies to modes 1-2.       */
     EIK_OPT_COLLECT_STATS = 3, /* 1 = count point updates/writes/sweeps on device [1]           */
-    EIK_OPT_TIME_CELL_EVENTS = 4, /* 1 = (host loop mode only) bracket every cell-sweep kernel
-                                    launch with CUDA events; sum in eik_stats.ms_cell_events [0] */
-    EIK_OPT_ASYNC_DEFER = 5, /* async mode readiness test on a popped cell: 0 none, 1 defer
-                                while a neighbour runs [1], 2 also while a neighbour is queued
-                                with a smaller key, 3 ... with a key smaller by > bin width     */
+    EIK_OPT_TIME_CELL_EVENTS = 4, /* 1 = (host loop and async modes) bracket every cell-sweep
+                                    kernel launch with CUDA events; sum in
+                                    eik_stats.ms_cell_events [0]                                 */
+    EIK_OPT_ASYNC_DEFER = 5, /* async mode readiness test on a popped cell (it is re-queued if
+                                an adjacent cell blocks it): 0 none; 1 a neighbour is running;
+                                2 ... or is queued with a smaller (key, index); 3 ... with a key
+                                smaller by > bin width; 4 as 2 across inflow faces only; 5 ...
+                                or is queued from an older activation generation; 6 ... or is
+                                queued with a smaller (generation, key, index) [6]; 7 ... with a
+                                smaller (key, generation, index).  2, 6 and 7 are strict total
+                                orders: the smallest queued cell is never deferred              */
     EIK_OPT_MAX_SWEEPS = 6,  /* sweeps per cell processing before the cell saves its active
                                 points and re-queues itself (bounds the round length, which is
-                                the slowest cell's); 0 = until convergence [4]                   */
+                                the slowest cell's); 0 = until convergence; -1 = automatic: 4
+                                in the round modes, 0 in async mode [-1]                         */
     EIK_OPT_TIMEOUT_S = 7,   /* device-side watchdog: the scheduler loop stops and the solve
                                 returns EIK_EINTERNAL after this many seconds [120]              */
     EIK_OPT_KAPPA = 8,       /* early termination threshold kappa >= 0 [0 = exact].

@@ -33,11 +33,11 @@ struct eik_ctx {
     // options
     double bin_width = INFINITY;
     uint32_t max_rounds = 1000000000u;
-    int loop_mode = 2;
+    int loop_mode = 0;            // asynchronous persistent scheduler (see include/eik.h)
     int collect_stats = 1;
     int time_cell_events = 0;
-    int async_defer = 1;
-    int max_sweeps = 4;
+    int async_defer = 6;
+    int max_sweeps = -1;          // -1: automatic (0 in async mode, 4 in the round modes)
     double kappa = 0.0;
     int legacy_key = 0;
     double timeout_s = 120.0;
@@ -271,7 +271,7 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         ctx->time_cell_events = value != 0;
         return EIK_OK;
     case EIK_OPT_ASYNC_DEFER:
-        if (value < 0 || value > 5) return fail(ctx, EIK_EINVAL, "defer mode must be 0..5");
+        if (value < 0 || value > 7) return fail(ctx, EIK_EINVAL, "defer mode must be 0..7");
         ctx->async_defer = (int)value;
         return EIK_OK;
     case EIK_OPT_KAPPA:
@@ -287,7 +287,7 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         ctx->timeout_s = value;
         return EIK_OK;
     case EIK_OPT_MAX_SWEEPS:
-        if (!(value >= 0) || value > 1e6) return fail(ctx, EIK_EINVAL, "max sweeps must be >= 0");
+        if (!(value >= -1) || value > 1e6) return fail(ctx, EIK_EINVAL, "max sweeps must be >= -1");
         ctx->max_sweeps = (int)value;
         return EIK_OK;
     default:
@@ -432,9 +432,12 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     CK(cudaMemsetAsync(ctx->gen, 0, (size_t)J * 4, ctx->stream));
     k_seed_queue<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
-    if (r == 16) return launch_async<T, 16>(ctx, ca, grid);
-    if (r == 8) return launch_async<T, 8>(ctx, ca, grid);
-    return launch_async<T, 4>(ctx, ca, grid);
+    const bool te = ctx->time_cell_events != 0;   // CUDA events around the persistent launch
+    if (te) CK(cudaEventRecord(ctx->cev[0], ctx->stream));
+    int st = r == 16 ? launch_async<T, 16>(ctx, ca, grid) : r == 8 ? launch_async<T, 8>(ctx, ca, grid)
+                                                                 : launch_async<T, 4>(ctx, ca, grid);
+    if (te) CK(cudaEventRecord(ctx->cev[1], ctx->stream));
+    return st;
 }
 
 template <typename T>
@@ -710,7 +713,9 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.plane_tab = ctx->plane_tab[ri];
     ca.Vt = ctx->Vt;
     ca.Ht = ctx->Ht;
-    ca.max_sweeps = ctx->max_sweeps;
+    // automatic sweep cap: rounds last as long as their slowest processing, so the round modes
+    // bound it (4 sweeps); the async scheduler has no rounds to shorten (a cap only adds work)
+    ca.max_sweeps = ctx->max_sweeps >= 0 ? ctx->max_sweeps : (ctx->loop_mode == 0 ? 0 : 4);
     ca.cap = (uint32_t)J;
     ca.pend = ctx->pend;
     ca.pdir = ctx->pdir;
@@ -800,6 +805,16 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     S.ms_cell_device = hc.cell_ns * 1e-6;
     S.ms_cell_events = ctx->ms_cell_events;
     S.cell_launches = hc.cell_launches;
+    if (method < 0 && ctx->loop_mode == 0 && hc.t_end > hc.t_start) {
+        // async: one persistent launch; its span is the first CTA's start to the last CTA's end
+        S.ms_cell_device = (hc.t_end - hc.t_start) * 1e-6;
+        S.cell_launches = 1;
+        if (ctx->time_cell_events) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ctx->cev[0], ctx->cev[1]);
+            S.ms_cell_events = ms;
+        }
+    }
     if (method >= 0) {
         S.grid_sweeps = hc.sweep_idx;
         S.cell_launches = (uint64_t)hc.sweep_idx * (uint64_t)(3 * cps - 2);

@@ -508,6 +508,9 @@ template <int R> struct CellCfg {
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
 template <typename T, int R> struct MinBlocks { static constexpr int value = CellCfg<R>::MINB; };
+// Five fp32 r = 16 CTAs fit an SM only while dynamic + static shared memory, rounded up to the
+// 128-byte allocation unit, plus the 1 KB per-CTA reservation, stays <= 228 KB / 5: 16 more
+// bytes of CellShared once dropped all three cell kernels to 4 CTAs per SM (checked below).
 template <> struct MinBlocks<float, 16> { static constexpr int value = EIK_MINB16; };
 template <> struct MinBlocks<double, 16> { static constexpr int value = 2; };
 
@@ -589,10 +592,14 @@ template <int R> struct CellShared {
     int32_t lcnt[2], lover;            // active-list lengths / overflow
     uint32_t bwd[2];                   // axes with activations behind the wavefront
     unsigned long long plane0;         // active planes of the first sweep (direction dir0)
-    long long tm[8];                   // phase timers (thread 0 only; diagnostics)
+    uint32_t tm[8];                    // phase timers (thread 0 only; diagnostics; clock mod 2^32)
     uint32_t nsteps;                   // plane steps of this processing (diagnostics)
     uint32_t dstate;                   // direction state saved at a sweep cap (pdir[c])
 };
+
+static_assert(((cell_smem_bytes<float, 16>() + sizeof(CellShared<16>) + 16 + 127) / 128 * 128 + 1024) * 5
+                  <= 228 * 1024,
+              "fp32 r = 16 cell kernels no longer fit 5 CTAs per SM (shared memory)");
 
 // dynamic shared memory carve-up
 template <typename T, int R> struct CellSmem {
@@ -919,7 +926,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // phase timers live in shared memory, written by thread 0 only (no registers held
     // across the sweeps): tm = {start, tile staged, halo staged, init done, mask, steps, list
     // iterations, face summaries start}
-    if (tid == 0) { S.tm[0] = clock64(); S.tm[4] = 0; S.tm[5] = 0; S.tm[6] = 0; }
+    if (tid == 0) { S.tm[0] = (uint32_t)clock64(); S.tm[4] = 0; S.tm[5] = 0; S.tm[6] = 0; }
     uint32_t nsteps = 0;
     constexpr int NWB = R3 / 32;   // saved-bitmask words
 
@@ -931,41 +938,22 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         // neighbour's re-activation of this cell may be consumed by this very processing in
         // fused rounds, hence the halo from L2)
         stage_cell_async<T, R>(Vt, Ht, sV, sH, c, cx, cy, cz, cps, A.cap);
-        if (tid == 0) S.tm[1] = clock64();
+        if (tid == 0) S.tm[1] = (uint32_t)clock64();
     } else {
+        // Async mode: a cell's tile may have been written by a CTA on another SM since this
+        // SM last cached it, so V comes through L2 only (16-byte .cg vector loads into
+        // registers).  hf is read-only during the solve: cp.async (no registers).  The halo
+        // loads are issued before the tile batches, all in one memory round trip.
         using V4 = typename Vec16<T>::type;
         constexpr int EL = 16 / sizeof(T);                // elements per vector
         constexpr int NV = R3 / EL;                       // vectors per tile
         constexpr int PV = (NV + NT - 1) / NT;            // vectors per thread
         constexpr int B = sizeof(T) == 4 ? 3 : 2;           // batch (register budget)
         const V4* Vt4 = reinterpret_cast<const V4*>(Vt + base);
-        const V4* Ht4 = reinterpret_cast<const V4*>(Ht + base);
-        V4* sH4 = reinterpret_cast<V4*>(sH);
-#pragma unroll
-        for (int m0 = 0; m0 < PV; m0 += B) {
-            V4 va[B], ha[B];
-#pragma unroll
-            for (int m = 0; m < B; ++m) {
-                const int vi = tid + (m0 + m) * NT;
-                if (m0 + m < PV && vi < NV) { va[m] = __ldcg(&Vt4[vi]); ha[m] = __ldcg(&Ht4[vi]); }
-            }
-#pragma unroll
-            for (int m = 0; m < B; ++m) {
-                const int vi = tid + (m0 + m) * NT;
-                if (m0 + m < PV && vi < NV) {
-                    sH4[vi] = ha[m];
-                    const T* pv = reinterpret_cast<const T*>(&va[m]);
-#pragma unroll
-                    for (int l = 0; l < EL; ++l) {
-                        const int e = vi * EL + l;
-                        const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
-                        sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = pv[l];
-                    }
-                }
-            }
+        {
+            const uint32_t hsb = smem_u32(sH);
+            for (int vi = tid; vi < NV; vi += NT) cp_async16(hsb + vi * 16, Ht + base + vi * EL);
         }
-        __syncthreads();
-        if (tid == 0) S.tm[1] = clock64();
         constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
         T hv[PH];
         int hq[PH];
@@ -993,8 +981,32 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             }
         }
 #pragma unroll
+        for (int m0 = 0; m0 < PV; m0 += B) {
+            V4 va[B];
+#pragma unroll
+            for (int m = 0; m < B; ++m) {
+                const int vi = tid + (m0 + m) * NT;
+                if (m0 + m < PV && vi < NV) va[m] = __ldcg(&Vt4[vi]);
+            }
+#pragma unroll
+            for (int m = 0; m < B; ++m) {
+                const int vi = tid + (m0 + m) * NT;
+                if (m0 + m < PV && vi < NV) {
+                    const T* pv = reinterpret_cast<const T*>(&va[m]);
+#pragma unroll
+                    for (int l = 0; l < EL; ++l) {
+                        const int e = vi * EL + l;
+                        const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+                        sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)] = pv[l];
+                    }
+                }
+            }
+        }
+#pragma unroll
         for (int m = 0; m < PH; ++m)
             if (hq[m] >= 0) sV[hq[m]] = hv[m];
+        cp_async_wait_all();
+        if (tid == 0) S.tm[1] = (uint32_t)clock64();
     }
     __syncthreads();
     // ---- initial activity: all points (INIT), or the points of the inflow faces whose
@@ -1002,7 +1014,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     // points saved at a sweep cap.  The first sweep's direction is fixed by the inflow faces,
     // so its set of active planes is collected here (no separate scan) ----
     __syncthreads();
-    if (tid == 0) S.tm[2] = clock64();
+    if (tid == 0) S.tm[2] = (uint32_t)clock64();
     // Sweep-direction state.  A continuation after a sweep cap resumes the direction sequence
     // where the capped processing left it (the saved word holds the direction chosen for the
     // sweep it did not run, the Gray-cycle position and the age of each axis' last reversal);
@@ -1076,7 +1088,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         if ((tid & 31) == 0 && cnt) { atomicAdd(&S.nact, cnt); atomicOr(&S.plane0, pm0); }
     }
     __syncthreads();
-    if (tid == 0) S.tm[3] = clock64();
+    if (tid == 0) S.tm[3] = (uint32_t)clock64();
 
     int prev_dir = -1;
     bool ran_list = false;
@@ -1166,7 +1178,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 cur ^= 1;
                 __syncthreads();
             }
-            if (tid == 0) S.tm[5] += clock64() - tl0;
+            if (tid == 0) S.tm[5] += (uint32_t)(clock64() - tl0);
             if (!overflow) break;          // converged in list mode
             nact = LCAP + 1;               // resume wavefront sweeps (flags authoritative)
         }
@@ -1230,7 +1242,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         nact = first ? S.nact : S.nact2[sw & 1];
         if (tid == 0) { S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0; }
         const long long tm1 = tid == 0 ? clock64() : 0;
-        if (tid == 0) S.tm[4] += tm1 - tm0;
+        if (tid == 0) S.tm[4] += (uint32_t)(tm1 - tm0);
         if (pm == 0ull) break;
         if (nact <= LCAP && sw > 0) continue;   // few left: list mode (next iteration)
         if (A.max_sweeps > 0 && nsweeps >= (uint32_t)A.max_sweeps) {
@@ -1277,13 +1289,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             default: bwd = sweep_dir<T, R, 7>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
             }
         }
-        if (tid == 0) S.tm[5] += clock64() - tm1;
+        if (tid == 0) S.tm[5] += (uint32_t)(clock64() - tm1);
         nact = LCAP + 1;   // unknown until the next scan
         for (int o = 16; o > 0; o >>= 1) bwd |= __shfl_xor_sync(0xffffffffu, bwd, o);
         if ((tid & 31) == 0 && bwd) atomicOr(&S.bwd[sw & 1], bwd);
         __syncthreads();
     }
-    if (tid == 0) S.tm[7] = clock64();
+    if (tid == 0) S.tm[7] = (uint32_t)clock64();
     // ---- face summaries (Eq. (3)): face f is currently downwind iff a border
     // point changed in this processing and ended below its outside neighbour (the staged
     // halo value, an upper bound of the current one: P:718 redundant tags are harmless); the
@@ -1351,12 +1363,12 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     }
     n_sweeps_out = nsweeps;
     if (tid == 0 && A.stats) {
-        atomicAdd(&A.ctl->dbg[36], (unsigned long long)(S.tm[3] - S.tm[0]));
-        atomicAdd(&A.ctl->dbg[41], (unsigned long long)(S.tm[1] - S.tm[0]));
-        atomicAdd(&A.ctl->dbg[42], (unsigned long long)(S.tm[2] - S.tm[1]));
+        atomicAdd(&A.ctl->dbg[36], (unsigned long long)(uint32_t)(S.tm[3] - S.tm[0]));
+        atomicAdd(&A.ctl->dbg[41], (unsigned long long)(uint32_t)(S.tm[1] - S.tm[0]));
+        atomicAdd(&A.ctl->dbg[42], (unsigned long long)(uint32_t)(S.tm[2] - S.tm[1]));
         atomicAdd(&A.ctl->dbg[37], (unsigned long long)S.tm[4]);
         atomicAdd(&A.ctl->dbg[38], (unsigned long long)S.tm[5]);
-        atomicAdd(&A.ctl->dbg[39], (unsigned long long)(clock64() - S.tm[7]));
+        atomicAdd(&A.ctl->dbg[39], (unsigned long long)(uint32_t)((uint32_t)clock64() - S.tm[7]));
         atomicAdd(&A.ctl->dbg[2], (unsigned long long)nsteps);
         S.nsteps = nsteps;
         atomicAdd(&A.ctl->dbg[40], (unsigned long long)S.tm[6]);
@@ -1567,55 +1579,69 @@ k_async(CellArgs A)
     for (;;) {
         if (tid == 0) {
             uint32_t got = Q_EMPTY, fl = 0;
-            unsigned ns = 32;
             for (;;) {
                 if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) break;
-                if (gtimer() - __ldcg(&ctl->t_solve0) > __ldcg(&ctl->budget_ns)) {   // watchdog
-                    atomicOr(&ctl->err, 8u);
-                    atomicExch(&ctl->abort, 1u);
-                    break;
-                }
-                const uint32_t h = __ldcg(&ctl->q_head), t = __ldcg(&ctl->q_tail);
-                if ((int32_t)(t - h) > 0) {   // never claim past the tail (the two loads are unordered)
-                    if (atomicCAS(&ctl->q_head, h, h + 1u) == h) {
-                        uint32_t v;
-                        while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) __nanosleep(20);
-                        EIK_CHECK(v < A.cap, "ring cell id");
-                        // readiness (the heap order of Alg. 3 approximated locally): defer v
-                        // while an adjacent cell is running or is queued with a smaller key
-                        // (ties broken by index, so the minimum is never deferred)
-                        const uint32_t kv = __ldcg(&A.key[v]);
-                        const uint32_t sv = __ldcg(&A.state[v]);
-                        bool defer = false;
-                        for (int f = 0; f < 6 && !defer; ++f) {
-                            // mode 4: only neighbours across an inflow face of v matter
-                            if (A.defer == 4 && !(sv & (1u << f))) continue;
-                            const int64_t nb = face_neighbour(v, f, A.cps);
-                            if (nb < 0) continue;
-                            const uint32_t sn = __ldcg(&A.state[nb]);
-                            if (sn & ST_RUNNING) defer = true;
-                            else if ((sn & ST_QUEUED) && A.defer == 5)
-                                defer = __ldcg(&A.gen[nb]) < __ldcg(&A.gen[v]);
-                            else if ((sn & ST_QUEUED) && (A.defer == 2 || A.defer == 3)) {
-                                const uint32_t kn = __ldcg(&A.key[nb]);
-                                if (A.defer == 2) defer = kn < kv || (kn == kv && (uint32_t)nb < v);
-                                else defer = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
-                            }
-                        }
-                        if (defer && A.defer) {
-                            const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & A.qmask;
-                            while (atomicCAS(&ring[slot], Q_EMPTY, v) != Q_EMPTY) __nanosleep(32);
-                            atomicAdd(&ctl->defers, 1ull);
-                            __nanosleep(64);
-                            continue;
-                        }
-                        got = v;
+                // ticket pop: every CTA takes the next head index with one atomicAdd (no CAS
+                // retry loop, which serialises 700+ CTAs to one claim per L2 round trip) and
+                // waits until the push of the same index has filled the slot, or the solve
+                // is over (pending = 0: no push will come)
+                const uint32_t h = atomicAdd(&ctl->q_head, 1u);
+                uint32_t v;
+                unsigned ns = 32;
+                bool quit = false;
+                while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) {
+                    if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) { quit = true; break; }
+                    if (gtimer() - __ldcg(&ctl->t_solve0) > __ldcg(&ctl->budget_ns)) {   // watchdog
+                        atomicOr(&ctl->err, 8u);
+                        atomicExch(&ctl->abort, 1u);
+                        quit = true;
                         break;
                     }
-                } else {
                     __nanosleep(ns);
                     ns = ns < 1024 ? ns * 2 : 1024;
                 }
+                if (quit) break;
+                EIK_CHECK(v < A.cap, "ring cell id");
+                // readiness (the heap order of Alg. 3 approximated locally): defer v while an
+                // adjacent cell is running or is queued with a smaller key (ties broken by
+                // index, so the minimum is never deferred)
+                const uint32_t kv = __ldcg(&A.key[v]);
+                const uint32_t sv = __ldcg(&A.state[v]);
+                bool defer = false;
+                for (int f = 0; f < 6 && !defer; ++f) {
+                    // mode 4: only neighbours across an inflow face of v matter
+                    if (A.defer == 4 && !(sv & (1u << f))) continue;
+                    const int64_t nb = face_neighbour(v, f, A.cps);
+                    if (nb < 0) continue;
+                    const uint32_t sn = __ldcg(&A.state[nb]);
+                    if (sn & ST_RUNNING) defer = true;
+                    else if ((sn & ST_QUEUED) && A.defer == 5)
+                        defer = __ldcg(&A.gen[nb]) < __ldcg(&A.gen[v]);
+                    else if ((sn & ST_QUEUED) && (A.defer == 6 || A.defer == 7)) {
+                        // a strict total order (no deferral cycles): 6 = (generation, key,
+                        // index), 7 = (key, generation, index)
+                        const uint32_t kn = __ldcg(&A.key[nb]);
+                        const uint32_t gn = __ldcg(&A.gen[nb]), gv = __ldcg(&A.gen[v]);
+                        if (A.defer == 6)
+                            defer = gn < gv || (gn == gv && (kn < kv || (kn == kv && (uint32_t)nb < v)));
+                        else
+                            defer = kn < kv || (kn == kv && (gn < gv || (gn == gv && (uint32_t)nb < v)));
+                    }
+                    else if ((sn & ST_QUEUED) && (A.defer == 2 || A.defer == 3)) {
+                        const uint32_t kn = __ldcg(&A.key[nb]);
+                        if (A.defer == 2) defer = kn < kv || (kn == kv && (uint32_t)nb < v);
+                        else defer = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
+                    }
+                }
+                if (defer && A.defer) {
+                    const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & A.qmask;
+                    while (atomicCAS(&ring[slot], Q_EMPTY, v) != Q_EMPTY) __nanosleep(32);
+                    atomicAdd(&ctl->defers, 1ull);
+                    __nanosleep(64);
+                    continue;
+                }
+                got = v;
+                break;
             }
             if (got != Q_EMPTY) {
                 fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
@@ -1642,7 +1668,7 @@ k_async(CellArgs A)
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
                 atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
-                if (A.defer == 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
+                if (A.defer >= 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
                 if (!(old & (ST_QUEUED | ST_RUNNING))) q_push(ctl, ring, A.qmask, (uint32_t)nc);
             }

@@ -151,7 +151,7 @@ def test_option_change_between_solves_takes_effect():
     sweep cap) must invalidate it, and a grid with the same cell count but another n must not
     reuse stale geometry."""
     import paper_1306_4743_b200 as eik
-    s = eik.Solver(device=0)
+    s = eik.Solver(device=0, loop_mode=2)
     w = W.c3(64)
     s.set_option(eik.EIK_OPT_MAX_SWEEPS, 0)
     _gpu(s, w, np.float32, 16)

@@ -51,7 +51,7 @@ out["launch_list"] = [{"kernel": k, "launches_profiled": agg[k][0], "us_per_laun
 ids = collections.defaultdict(dict)
 for d in rows_of(kmet):
     ids[int(d["ID"])][d["Metric Name"]] = val(d)
-last = sorted(ids)[-rounds:]
+last = sorted(ids)[-max(rounds, 1):]   # async (rounds = 0): the one k_async launch
 byts = collections.defaultdict(float)
 for i in last:
     for m, v in ids[i].items():

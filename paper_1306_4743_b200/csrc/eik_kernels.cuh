@@ -1577,80 +1577,84 @@ k_async(CellArgs A)
     uint32_t* ring = A.wl0;
     if (tid == 0) atomicMin(&ctl->t_start, gtimer());
     for (;;) {
-        if (tid == 0) {
+        if (tid < 32) {   // warp 0 pops the next cell; the other warps wait at the barrier
+            const int lane = tid;
             uint32_t got = Q_EMPTY, fl = 0;
             for (;;) {
-                if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) break;
-                // ticket pop: every CTA takes the next head index with one atomicAdd (no CAS
-                // retry loop, which serialises 700+ CTAs to one claim per L2 round trip) and
-                // waits until the push of the same index has filled the slot, or the solve
-                // is over (pending = 0: no push will come)
-                const uint32_t h = atomicAdd(&ctl->q_head, 1u);
-                uint32_t v;
-                unsigned ns = 32;
-                bool quit = false;
-                while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) {
-                    if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) { quit = true; break; }
-                    if (gtimer() - __ldcg(&ctl->t_solve0) > __ldcg(&ctl->budget_ns)) {   // watchdog
-                        atomicOr(&ctl->err, 8u);
-                        atomicExch(&ctl->abort, 1u);
-                        quit = true;
-                        break;
+                // lane 0: ticket pop -- every CTA takes the next head index with one atomicAdd
+                // (no CAS retry loop, which serialises 700+ CTAs to one claim per L2 round
+                // trip) and waits until the push of the same index has filled the slot, or the
+                // solve is over (pending = 0: no push will come)
+                uint32_t v = Q_EMPTY;
+                int quit = 0;
+                if (lane == 0) {
+                    if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) quit = 1;
+                    if (!quit) {
+                        const uint32_t h = atomicAdd(&ctl->q_head, 1u);
+                        unsigned ns = 32;
+                        while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) {
+                            if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) { quit = 1; break; }
+                            if (gtimer() - __ldcg(&ctl->t_solve0) > __ldcg(&ctl->budget_ns)) {   // watchdog
+                                atomicOr(&ctl->err, 8u);
+                                atomicExch(&ctl->abort, 1u);
+                                quit = 1;
+                                break;
+                            }
+                            __nanosleep(ns);
+                            ns = ns < 1024 ? ns * 2 : 1024;
+                        }
                     }
-                    __nanosleep(ns);
-                    ns = ns < 1024 ? ns * 2 : 1024;
                 }
+                quit = __shfl_sync(0xffffffffu, quit, 0);
                 if (quit) break;
+                v = __shfl_sync(0xffffffffu, v, 0);
                 EIK_CHECK(v < A.cap, "ring cell id");
-                // readiness (the heap order of Alg. 3 approximated locally): defer v while an
-                // adjacent cell is running or is queued with a smaller key (ties broken by
-                // index, so the minimum is never deferred)
-                const uint32_t kv = __ldcg(&A.key[v]);
-                const uint32_t sv = __ldcg(&A.state[v]);
-                bool defer = false;
-                for (int f = 0; f < 6 && !defer; ++f) {
+                // readiness (the heap order of Alg. 3 approximated locally): lane f checks the
+                // neighbour across face f -- all loads of the six checks in one round trip --
+                // and v is re-queued while a neighbour runs or is queued ahead of it
+                bool d = false;
+                if (A.defer && lane < 6) {
+                    const int64_t nb = face_neighbour(v, lane, A.cps);
+                    const uint32_t kv = __ldcg(&A.key[v]), sv = __ldcg(&A.state[v]), gv = __ldcg(&A.gen[v]);
+                    uint32_t sn = 0, kn = KEY_INF, gn = 0;
+                    if (nb >= 0) { sn = __ldcg(&A.state[nb]); kn = __ldcg(&A.key[nb]); gn = __ldcg(&A.gen[nb]); }
                     // mode 4: only neighbours across an inflow face of v matter
-                    if (A.defer == 4 && !(sv & (1u << f))) continue;
-                    const int64_t nb = face_neighbour(v, f, A.cps);
-                    if (nb < 0) continue;
-                    const uint32_t sn = __ldcg(&A.state[nb]);
-                    if (sn & ST_RUNNING) defer = true;
-                    else if ((sn & ST_QUEUED) && A.defer == 5)
-                        defer = __ldcg(&A.gen[nb]) < __ldcg(&A.gen[v]);
-                    else if ((sn & ST_QUEUED) && (A.defer == 6 || A.defer == 7)) {
-                        // a strict total order (no deferral cycles): 6 = (generation, key,
-                        // index), 7 = (key, generation, index)
-                        const uint32_t kn = __ldcg(&A.key[nb]);
-                        const uint32_t gn = __ldcg(&A.gen[nb]), gv = __ldcg(&A.gen[v]);
-                        if (A.defer == 6)
-                            defer = gn < gv || (gn == gv && (kn < kv || (kn == kv && (uint32_t)nb < v)));
-                        else
-                            defer = kn < kv || (kn == kv && (gn < gv || (gn == gv && (uint32_t)nb < v)));
-                    }
-                    else if ((sn & ST_QUEUED) && (A.defer == 2 || A.defer == 3)) {
-                        const uint32_t kn = __ldcg(&A.key[nb]);
-                        if (A.defer == 2) defer = kn < kv || (kn == kv && (uint32_t)nb < v);
-                        else defer = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
+                    if (nb >= 0 && !(A.defer == 4 && !(sv & (1u << lane)))) {
+                        if (sn & ST_RUNNING) d = true;
+                        else if (sn & ST_QUEUED) {
+                            if (A.defer == 5) d = gn < gv;
+                            else if (A.defer == 2) d = kn < kv || (kn == kv && (uint32_t)nb < v);
+                            else if (A.defer == 3) d = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
+                            else if (A.defer == 6)   // strict total order (no deferral cycles)
+                                d = gn < gv || (gn == gv && (kn < kv || (kn == kv && (uint32_t)nb < v)));
+                            else if (A.defer == 7)
+                                d = kn < kv || (kn == kv && (gn < gv || (gn == gv && (uint32_t)nb < v)));
+                        }
                     }
                 }
-                if (defer && A.defer) {
-                    const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & A.qmask;
-                    while (atomicCAS(&ring[slot], Q_EMPTY, v) != Q_EMPTY) __nanosleep(32);
-                    atomicAdd(&ctl->defers, 1ull);
-                    __nanosleep(64);
+                if (__any_sync(0xffffffffu, d)) {
+                    if (lane == 0) {
+                        const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & A.qmask;
+                        while (atomicCAS(&ring[slot], Q_EMPTY, v) != Q_EMPTY) __nanosleep(32);
+                        atomicAdd(&ctl->defers, 1ull);
+                        __nanosleep(64);
+                    }
+                    __syncwarp();
                     continue;
                 }
                 got = v;
                 break;
             }
-            if (got != Q_EMPTY) {
-                fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
-                if (!A.legacy_key) A.key[got] = KEY_INF;             // V^c <- +inf
-                __threadfence();
+            if (lane == 0) {
+                if (got != Q_EMPTY) {
+                    fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
+                    if (!A.legacy_key) A.key[got] = KEY_INF;             // V^c <- +inf
+                    __threadfence();
+                }
+                S.cell = got;
+                S.flags = fl;
+                S.stat[0] = S.stat[1] = S.stat[2] = 0;
             }
-            S.cell = got;
-            S.flags = fl;
-            S.stat[0] = S.stat[1] = S.stat[2] = 0;
         }
         __syncthreads();
         const uint32_t c = S.cell;
@@ -1660,22 +1664,26 @@ k_async(CellArgs A)
         cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
         __threadfence();   // value stores before the re-activations
         __syncthreads();
-        if (S.cont && tid == 7) {
-            __stcg(&A.pdir[c], S.dstate);
-            __threadfence();   // before the cell is re-queued below
-        }
+        // re-activations first, then the cell's own release: a neighbour waiting for this
+        // cell to stop running must find its tag already set (releasing first let it run
+        // without the tag and then again with it: 50 % more processings on C4)
         if (tid < 6 && (S.face_flag & (1u << tid))) {
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
                 atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
                 if (A.defer >= 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
-                if (!(old & (ST_QUEUED | ST_RUNNING))) q_push(ctl, ring, A.qmask, (uint32_t)nc);
+                if (!(old & (ST_QUEUED | ST_RUNNING))) {
+                    q_push(ctl, ring, A.qmask, (uint32_t)nc);
+                    __threadfence();   // the push's pending increment before this cell's decrement
+                }
             }
         }
         __syncthreads();
         if (tid == 0) {
-            if (S.cont) {
+            if (S.cont) {   // sweep cap: save the direction state, continue later
+                __stcg(&A.pdir[c], S.dstate);
+                __threadfence();   // before the cell is re-queued below
                 atomicMin(&A.key[c], S.cont_key);
                 atomicOr(&A.state[c], FLAG_CONT | ST_QUEUED);
             }

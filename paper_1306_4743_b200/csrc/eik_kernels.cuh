@@ -1649,7 +1649,8 @@ k_async(CellArgs A)
                 if (got != Q_EMPTY) {
                     fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
                     if (!A.legacy_key) A.key[got] = KEY_INF;             // V^c <- +inf
-                    __threadfence();
+                    // (no fence: the tile loads depend on `got`, which was read from the ring
+                    // after its producer fenced the cell's values, and go to L2)
                 }
                 S.cell = got;
                 S.flags = fl;

@@ -130,6 +130,22 @@ __device__ __forceinline__ T local_solve(T mx, T my, T mz, T hf)
     return a1 + t;
 }
 
+// min / max of non-NaN values (every operand here is >= 0 or +inf, or a clamped difference):
+// fp64 as one compare and two selects, without the NaN fix-up fmin/fmax compile to
+// (DSETP.MIN + FSEL + SEL + LOP3 and register moves); fp32 keeps FMNMX
+#ifndef EIK_VMIN
+#define EIK_VMIN 1
+#endif
+__device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
+#if EIK_VMIN
+__device__ __forceinline__ double vmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double vmax(double a, double b) { return b > a ? b : a; }
+#else
+__device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
+#endif
+
 // The same solve with the two- and three-sided candidates evaluated side by side and then
 // selected (shorter dependent chain: both square roots issue together).  d2, d3 are clamped to
 // hf, which changes nothing when a branch is taken (it requires d2 < hf, resp. d3 < t2 <= hf)
@@ -150,16 +166,16 @@ __device__ __forceinline__ double sqrt_approx(double x) { return __dsqrt_rn(x); 
 template <typename T>
 __device__ __forceinline__ T local_solve_fast(T mx, T my, T mz, T hf)
 {
-    const T lo = fmin(mx, my), hi = fmax(mx, my);
-    const T a1 = fmin(lo, mz);
-    const T a3 = fmax(hi, mz);
-    const T a2 = fmax(lo, fmin(hi, mz));
-    const T d2 = fmin(a2 - a1, hf);
-    const T d3 = fmin(a3 - a1, hf);
+    const T lo = vmin(mx, my), hi = vmax(mx, my);
+    const T a1 = vmin(lo, mz);
+    const T a3 = vmax(hi, mz);
+    const T a2 = vmax(lo, vmin(hi, mz));
+    const T d2 = vmin(a2 - a1, hf);
+    const T d3 = vmin(a3 - a1, hf);
     const T hh = hf * hf;
-    const T t2 = (d2 + sqrt_approx(fmax(T(2) * hh - d2 * d2, T(0)))) * T(0.5);
+    const T t2 = (d2 + sqrt_approx(vmax(T(2) * hh - d2 * d2, T(0)))) * T(0.5);
     const T e = d3 - d2;
-    const T t3 = (d2 + d3 + sqrt_approx(fmax(T(3) * hh - (d2 * d2 + d3 * d3 + e * e), T(0)))) * T(1.0 / 3.0);
+    const T t3 = (d2 + d3 + sqrt_approx(vmax(T(3) * hh - (d2 * d2 + d3 * d3 + e * e), T(0)))) * T(1.0 / 3.0);
     T t = hf;
     if (hf > d2) t = (t2 > d3) ? t3 : t2;
     return a1 + t;
@@ -690,9 +706,9 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                 const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
                 const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
                 const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
-                const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
+                const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
                 const T hf = fabs(hs);
-                if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
+                if (hf < INF && vmin(mx, vmin(my, mz)) < v) {
                     ++nupd;
                     const T u = local_solve_fast<T>(mx, my, mz, hf);
                     if (u < v) {
@@ -701,7 +717,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                         ++nwr;
                         // kappa: a change <= kappa activates nothing (ut = +inf)
                         const T ut = (v - u > kap) ? u : INF;
-                        dmax = fmax(dmax, v - u);
+                        dmax = vmax(dmax, v - u);
                         const unsigned ca = ue & (R - 1), cb = (ue / R) & (R - 1), cc = ue / (R * R);
                         const int bxa = (xb > ut) & (ca > 0), bya = (yb > ut) & (cb > 0), bza = (zb > ut) & (cc > 0);
                         sts_u8(bxa ? ab + up - oxp : scratch, 1u);
@@ -739,9 +755,9 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
             const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
             if (fl) {
                 sts_u8(ab + up, 0u);                                   // Alg. 2 line 4
-                const T mx = fmin(xf, xb), my = fmin(yf, yb), mz = fmin(zf, zb);
+                const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
                 const T hf = fabs(hs);
-                if (hf < INF && fmin(mx, fmin(my, mz)) < v) {          // fixed / no gain
+                if (hf < INF && vmin(mx, vmin(my, mz)) < v) {          // fixed / no gain
                     ++nupd;
                     const T u = local_solve_fast<T>(mx, my, mz, hf);    // line 5
                     if (u < v) {                                         // line 6
@@ -1137,8 +1153,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                     const T xm = sV[q - 1], xp = sV[q + 1];
                     const T ym = sV[q - RP], yp = sV[q + RP];
                     const T zm = sV[q - RP2], zp = sV[q + RP2];
-                    const T mx = fmin(xm, xp), my = fmin(ym, yp), mz = fmin(zm, zp);
-                    if (hf < INF && fmin(mx, fmin(my, mz)) < v) {
+                    const T mx = vmin(xm, xp), my = vmin(ym, yp), mz = vmin(zm, zp);
+                    if (hf < INF && vmin(mx, vmin(my, mz)) < v) {
                         ++nupd;
                         const T u = local_solve_fast<T>(mx, my, mz, hf);      // line 5
                         if (u < v) {                                          // line 6

@@ -79,6 +79,14 @@ class Clocks:
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
+        # wait for the first sample (nvidia-smi starts in ~0.1-1 s) so that the sampler is live
+        # when the timed region starts; a region of a few ms still gets the sample at its start
+        self.pre = ""
+        if self.p is not None:
+            import select
+            r, _, _ = select.select([self.p.stdout], [], [], 5.0)
+            if r:
+                self.pre = self.p.stdout.readline()
         return self
 
     def __exit__(self, *a):
@@ -93,7 +101,7 @@ class Clocks:
 
     def summary(self):
         rows = []
-        for line in (self.out or "").strip().splitlines():
+        for line in (self.pre + (self.out or "")).strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) == 6 and f[0].replace(".", "").isdigit():
                 rows.append(f)

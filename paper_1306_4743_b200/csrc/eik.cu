@@ -422,6 +422,9 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 4>, CellCfg<4>::NT, cell_smem_bytes<T, 4>());
     CK(e);
     if (occ < 1) occ = 1;
+#ifdef EIK_ASYNC_OCC_CAP
+    if (occ > EIK_ASYNC_OCC_CAP) occ = EIK_ASYNC_OCC_CAP;   // (experiment: fewer CTAs per SM)
+#endif
     // every CTA is co-resident (grid = occupancy x SMs): idle CTAs only poll the ring
     const int grid = occ * ctx->sm_count;
     ca.qmask = (uint32_t)(ctx->ring_cap - 1);

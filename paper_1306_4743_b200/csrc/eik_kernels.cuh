@@ -498,6 +498,9 @@ __global__ void k_round_end(Ctl* ctl) { (void)round_end_body(ctl); }
 // --------------------------------------------------------------------------------------
 // A3-A6: the cell-sweep kernel
 // --------------------------------------------------------------------------------------
+#ifndef EIK_MINB8
+#define EIK_MINB8 12   // measured (fp64 r = 8): 8 -> 12 P2 24.0 -> 21.5 ms, C2d 10.7 -> 10.5; 16 slower
+#endif
 template <int R> struct CellCfg {
     static constexpr int R3 = R * R * R;
     static constexpr int RP = R + 2;
@@ -507,7 +510,7 @@ template <int R> struct CellCfg {
     static constexpr int MAXP = R == 16 ? 192 : (R == 8 ? 48 : 12);  // largest plane
     static constexpr int PPT = 1;                                    // plane points / thread (2 measured slower)
     static constexpr int NT = ((MAXP + PPT - 1) / PPT + 31) / 32 * 32;
-    static constexpr int MINB = R == 16 ? 4 : 8;                     // CTAs per SM target
+    static constexpr int MINB = R == 16 ? 4 : EIK_MINB8;             // CTAs per SM target
     static constexpr int LCAP = R == 16 ? 384 : (R == 8 ? 128 : 64);  // active-list capacity
 };
 
@@ -528,12 +531,29 @@ template <typename T, int R> struct MinBlocks { static constexpr int value = Cel
 // 128-byte allocation unit, plus the 1 KB per-CTA reservation, stays <= 228 KB / 5: 16 more
 // bytes of CellShared once dropped all three cell kernels to 4 CTAs per SM (checked below).
 template <> struct MinBlocks<float, 16> { static constexpr int value = EIK_MINB16; };
+// fp64 r = 16 (EIK_HF_GLOBAL64): hf stays in global memory (read through L1/L2 one plane
+// ahead) and "changed" is a bitmask, so the shared-memory footprint drops from 85 to 53 KB
+// and the SM holds EIK_MINB64 CTAs instead of 2
+#ifndef EIK_HF_GLOBAL64
+#define EIK_HF_GLOBAL64 1
+#endif
+#ifndef EIK_MINB64
+#define EIK_MINB64 4   // measured: 2 (hf in shared memory) 29.6 ms on C3d, 3 26.2, 4 24.0
+#endif
+template <typename T, int R> struct HfGlobal { static constexpr bool value = false; };
+#if EIK_HF_GLOBAL64
+template <> struct HfGlobal<double, 16> { static constexpr bool value = true; };
+template <> struct MinBlocks<double, 16> { static constexpr int value = EIK_MINB64; };
+#else
 template <> struct MinBlocks<double, 16> { static constexpr int value = 2; };
+#endif
 
 template <typename T, int R>
 constexpr size_t cell_smem_bytes()
 {
-    // V box + hf + active bytes (+ scratch) + 2 active lists (uint16)
+    // V box + hf (or a changed bitmask) + active bytes (+ scratch) + 2 active lists (uint16)
+    if constexpr (HfGlobal<T, R>::value)
+        return sizeof(T) * CellCfg<R>::BOX + CellCfg<R>::R3 + 16 + CellCfg<R>::R3 / 8 + 4 * CellCfg<R>::LCAP;
     return sizeof(T) * (CellCfg<R>::BOX + CellCfg<R>::R3) + CellCfg<R>::R3 + 16 + 4 * CellCfg<R>::LCAP;
 }
 
@@ -619,16 +639,32 @@ static_assert(((cell_smem_bytes<float, 16>() + sizeof(CellShared<16>) + 16 + 127
 
 // dynamic shared memory carve-up
 template <typename T, int R> struct CellSmem {
+    static constexpr bool HG = HfGlobal<T, R>::value;
     T* V;          // (R+2)^3 box incl. halo faces
-    T* H;          // R^3 hf (sign bit set = point changed in this processing)
+    T* H;          // R^3 hf (sign bit set = point changed in this processing); null if HG
     uint8_t* act;  // R^3 active flags (Alg. 2)
+    uint32_t* chg; // HG: R^3 changed bits
     uint16_t* list; // 2 x LCAP active-point lists
+    const T* Hg;   // HG: this cell's hf tile in global memory (set per processing)
     __device__ explicit CellSmem(unsigned char* raw)
     {
         V = reinterpret_cast<T*>(raw);
-        H = V + CellCfg<R>::BOX;
-        act = reinterpret_cast<uint8_t*>(H + CellCfg<R>::R3);
-        list = reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3 + 16);   // act[R3] = scratch
+        H = HG ? nullptr : V + CellCfg<R>::BOX;
+        act = reinterpret_cast<uint8_t*>(V + CellCfg<R>::BOX + (HG ? 0 : CellCfg<R>::R3));
+        chg = HG ? reinterpret_cast<uint32_t*>(act + CellCfg<R>::R3 + 16) : nullptr;   // act[R3] = scratch
+        list = HG ? reinterpret_cast<uint16_t*>(chg + CellCfg<R>::R3 / 32)
+                  : reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3 + 16);
+        Hg = nullptr;
+    }
+    __device__ __forceinline__ T hf(int p) const { if constexpr (HG) return __ldg(Hg + p); else return H[p]; }
+    __device__ __forceinline__ bool changed(int p) const
+    {
+        if constexpr (HG) return (chg[p >> 5] >> (p & 31)) & 1u; else return H[p] < T(0);
+    }
+    __device__ __forceinline__ void mark(int p, T hs)
+    {
+        if constexpr (HG) atomicOr(&chg[p >> 5], 1u << (p & 31));
+        else if (hs > T(0)) H[p] = -hs;
     }
 };
 
@@ -655,7 +691,9 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     const T INF = dinf<T>();
     // shared-window bases: V box (at the first interior point), hf, activity bytes
     const uint32_t vb = smem_u32(M.V) + (uint32_t)((1 + RP + RP2) * TS);
-    const uint32_t hb = smem_u32(M.H);
+    constexpr bool HG = CellSmem<T, R>::HG;
+    const uint32_t hb = HG ? 0u : smem_u32(M.H);
+    const T* __restrict__ hg = M.Hg;
     const uint32_t ab = smem_u32(M.act);
     const uint32_t scratch = ab + R3;   // activity stores that do not apply go here
     bool fwd = false;
@@ -679,11 +717,12 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     const uint16_t* tp = ptab + tid;
     unsigned en = __ldg(&tp[s * NT]);
     unsigned en1 = __ldg(&tp[(s + 1) * NT]);
-    T hn = en < (unsigned)R3 ? lds<T>(hb + (en ^ dm) * TS) : INF;
+#define EIK_HFLD(e_) (HG ? __ldg(hg + (e_)) : lds<T>(hb + (e_) * TS))
+    T hn = en < (unsigned)R3 ? EIK_HFLD(en ^ dm) : INF;
 #define EIK_PREFETCH(sp_)                                                                  \
     {                                                                                  \
         en = en1;                                                                      \
-        hn = en < (unsigned)R3 ? lds<T>(hb + (en ^ dm) * TS) : INF;                    \
+        hn = en < (unsigned)R3 ? EIK_HFLD(en ^ dm) : INF;                              \
         en1 = __ldg(&tp[((sp_) + 1) * NT]);                                            \
     }
     // box byte offset of point p = a + R b + R^2 c (relative to vb)
@@ -713,7 +752,8 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                     const T u = local_solve_fast<T>(mx, my, mz, hf);
                     if (u < v) {
                         sts(qa, u);
-                        if (hs > T(0)) sts(hb + up * TS, -hs);
+                        if constexpr (HG) atomicOr(&M.chg[up >> 5], 1u << (up & 31));
+                        else if (hs > T(0)) sts(hb + up * TS, -hs);
                         ++nwr;
                         // kappa: a change <= kappa activates nothing (ut = +inf)
                         const T ut = (v - u > kap) ? u : INF;
@@ -762,7 +802,8 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                     const T u = local_solve_fast<T>(mx, my, mz, hf);    // line 5
                     if (u < v) {                                         // line 6
                         sts(qa, u);                                      // line 7
-                        if (hs > T(0)) sts(hb + up * TS, -hs);           // mark changed
+                        if constexpr (HG) atomicOr(&M.chg[up >> 5], 1u << (up & 31));   // mark changed
+                        else if (hs > T(0)) sts(hb + up * TS, -hs);
                         ++nwr;
                         // lines 8-13: activate larger in-cell neighbours (the cross-border
                         // "currently downwind" test is done once per processing)
@@ -791,6 +832,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     }
 #undef EIK_QOFF
 #undef EIK_PREFETCH
+#undef EIK_HFLD
     return bwd;
 }
 
@@ -803,7 +845,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
 // earlier in this launch on another SM may have changed it after this SM cached the lines.
 template <typename T, int R>
 __device__ __forceinline__ void stage_cell_async(const T* __restrict__ Vt, const T* __restrict__ Ht,
-                                                 T* sV, T* sH, uint32_t c, int cx, int cy, int cz,
+                                                 CellSmem<T, R>& M, uint32_t c, int cx, int cy, int cz,
                                                  int cps, uint32_t cap)
 {
     using C = CellCfg<R>;
@@ -812,9 +854,16 @@ __device__ __forceinline__ void stage_cell_async(const T* __restrict__ Vt, const
     const T INF = dinf<T>();
     const int64_t base = (int64_t)c * R3;
     (void)cap;
-    const uint32_t vs = smem_u32(sV), hs = smem_u32(sH);
+    T* sV = M.V;
+    const uint32_t vs = smem_u32(sV);
     constexpr int EL = 16 / sizeof(T);
-    for (int vi = tid; vi < R3 / EL; vi += NT) cp_async16(hs + vi * 16, Ht + base + vi * EL);
+    if constexpr (CellSmem<T, R>::HG) {
+        M.Hg = Ht + base;
+        for (int w = tid; w < R3 / 32; w += NT) M.chg[w] = 0u;
+    } else {
+        const uint32_t hs = smem_u32(M.H);
+        for (int vi = tid; vi < R3 / EL; vi += NT) cp_async16(hs + vi * 16, Ht + base + vi * EL);
+    }
     for (int e = tid; e < R3; e += NT) {
         const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
         cp_async_el(vs + ((a + 1) + RP * (b + 1) + RP2 * (d + 1)) * (int)sizeof(T), Vt + base + e);
@@ -855,8 +904,7 @@ __device__ __forceinline__ void stage_cell_async(const T* __restrict__ Vt, const
 // vector holding any changed point is stored whole (unchanged values are rewritten
 // identically).  Returns the number of changed points this thread wrote.
 template <typename T, int R>
-__device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__ Vc, const T* sV,
-                                                                 const T* sH)
+__device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__ Vc, const CellSmem<T, R>& M)
 {
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2;
@@ -865,13 +913,17 @@ __device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__
     constexpr int NV = R3 / EL;
     unsigned long long nw = 0;
     V4* Vt4 = reinterpret_cast<V4*>(Vc);
-    const V4* sH4 = reinterpret_cast<const V4*>(sH);
+    const T* sV = M.V;
     for (int vi = threadIdx.x; vi < NV; vi += NT) {
-        const V4 hv = sH4[vi];
-        const T* ph = reinterpret_cast<const T*>(&hv);
         int nchg = 0;
+        if constexpr (CellSmem<T, R>::HG) {
+            nchg = __popc((M.chg[(vi * EL) >> 5] >> ((vi * EL) & 31)) & ((1u << EL) - 1u));
+        } else {
+            const V4 hv = reinterpret_cast<const V4*>(M.H)[vi];
+            const T* ph = reinterpret_cast<const T*>(&hv);
 #pragma unroll
-        for (int l = 0; l < EL; ++l) nchg += ph[l] < T(0);
+            for (int l = 0; l < EL; ++l) nchg += ph[l] < T(0);
+        }
         if (nchg) {
             V4 out;
             T* po = reinterpret_cast<T*>(&out);
@@ -923,7 +975,6 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     T* Vt = reinterpret_cast<T*>(A.Vt);
     const T* Ht = reinterpret_cast<const T*>(A.Ht);
     T* sV = M.V;
-    T* sH = M.H;
     uint8_t* sA = M.act;
     const int cps = A.cps;
     const T INF = dinf<T>();
@@ -953,7 +1004,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         // Round mode: cp.async staging (see stage_cell_async; a round is one launch, and a
         // neighbour's re-activation of this cell may be consumed by this very processing in
         // fused rounds, hence the halo from L2)
-        stage_cell_async<T, R>(Vt, Ht, sV, sH, c, cx, cy, cz, cps, A.cap);
+        stage_cell_async<T, R>(Vt, Ht, M, c, cx, cy, cz, cps, A.cap);
         if (tid == 0) S.tm[1] = (uint32_t)clock64();
     } else {
         // Async mode: a cell's tile may have been written by a CTA on another SM since this
@@ -966,8 +1017,11 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         constexpr int PV = (NV + NT - 1) / NT;            // vectors per thread
         constexpr int B = sizeof(T) == 4 ? 3 : 2;           // batch (register budget)
         const V4* Vt4 = reinterpret_cast<const V4*>(Vt + base);
-        {
-            const uint32_t hsb = smem_u32(sH);
+        if constexpr (CellSmem<T, R>::HG) {
+            M.Hg = Ht + base;
+            for (int w = tid; w < R3 / 32; w += NT) M.chg[w] = 0u;
+        } else {
+            const uint32_t hsb = smem_u32(M.H);
             for (int vi = tid; vi < NV; vi += NT) cp_async16(hsb + vi * 16, Ht + base + vi * EL);
         }
         constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
@@ -1145,7 +1199,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                     const int p = Lc[t];
                     EIK_CHECK(p >= 0 && p < R3, "list point index");
                     sA[p] = 0;                                               // Alg. 2 line 4
-                    const T hs = sH[p];
+                    const T hs = M.hf(p);
                     const T hf = fabs(hs);
                     const int i = p % R, j = (p / R) % R, k = p / (R * R);
                     const int q = (i + 1) + RP * (j + 1) + RP2 * (k + 1);
@@ -1159,7 +1213,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                         const T u = local_solve_fast<T>(mx, my, mz, hf);      // line 5
                         if (u < v) {                                          // line 6
                             sV[q] = u;                                        // line 7
-                            if (hs > T(0)) sH[p] = -hs;
+                            M.mark(p, hs);
                             ++nwr;
                             // lines 8-10: claim larger neighbours (CAS on the flag word) and
                             // append them to the next list
@@ -1341,7 +1395,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 f_prev = f;
             }
             const int pp = a + R * b + R * R * d;
-            if (sH[pp] < T(0)) {
+            if (M.changed(pp)) {
                 const T val = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
                 const T out = sV[(ha + 1) + RP * (hb + 1) + RP2 * (hd + 1)];
                 // kappa: a border change <= kappa tags no neighbour cell (the tile in
@@ -1363,7 +1417,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 
     // ---- write back (16-byte vectors; a vector holding any changed point is stored whole,
     // unchanged values are rewritten identically) ----
-    unsigned long long nw = write_back_changed<T, R>(Vt + base, sV, sH);
+    unsigned long long nw = write_back_changed<T, R>(Vt + base, M);
     if (A.stats) {
         unsigned long long u64 = nupd, w64 = nwr;
         for (int o = 16; o > 0; o >>= 1) {
@@ -1783,7 +1837,7 @@ k_dsweep(CellArgs A, int D)
         __syncthreads();
         if (!S.cell) continue;
         ++nproc;
-        stage_cell_async<T, R>(Vt, Ht, Msm.V, Msm.H, c, cx, cy, cz, cps, A.cap);
+        stage_cell_async<T, R>(Vt, Ht, Msm, c, cx, cy, cz, cps, A.cap);
         __syncthreads();
         const unsigned long long pm = (1ull << NPL) - 1ull;   // every plane, no gating (FSM)
         if constexpr (R < EIK_DIR_TEMPLATE_MIN_R) {
@@ -1799,7 +1853,7 @@ k_dsweep(CellArgs A, int D)
         default: sweep_dir<T, R, 7>(S, Msm, A.plane_tab, pm, true, nupd, nwr, nsteps, kap, dmax); break;
         }
         // (sweep_dir ends with a barrier: every changed point carries the sign bit of hf)
-        unsigned long long nw = write_back_changed<T, R>(Vt + (int64_t)c * R3, Msm.V, Msm.H);
+        unsigned long long nw = write_back_changed<T, R>(Vt + (int64_t)c * R3, Msm);
         if (A.locked) {
             // faces holding a changed point: the neighbour across them must run next time
             uint32_t fm = 0;
@@ -1814,7 +1868,7 @@ k_dsweep(CellArgs A, int D)
                 case 4: pa = u; pb = v; pd = 0; break;
                 default: pa = u; pb = v; pd = R - 1; break;
                 }
-                if (Msm.H[pa + R * pb + R * R * pd] < T(0)) fm |= 1u << f;
+                if (Msm.changed(pa + R * pb + R * R * pd)) fm |= 1u << f;
             }
             for (int o = 16; o > 0; o >>= 1) fm |= __shfl_xor_sync(0xffffffffu, fm, o);
             if ((tid & 31) == 0 && fm) atomicOr(&S.face_flag, fm);

@@ -357,10 +357,14 @@ def main():
         for _ in range(args.e2e_steps):
             solver.solve_host(Fh, mh, qh, h=grid_h(cfg, n), cell_size=r, n=n, out=Uh)
         t_e = job_time((time.perf_counter() - t0) / args.e2e_steps, pg, dev)
+        st_h = solver.stats()   # bytes the C call moved (F and mask copied; exit_vals read in
+        # place at the exits: page-locked host memory, mapped)
         e2e = {"value": job_value(M, ws, t_e), "unit": UNIT, "ms_per_step": t_e * 1e3,
-               "h2d_bytes_per_step": int(Fh.numel() * Fh.element_size() + mh.numel() + qh.numel() * qh.element_size()),
-               "d2h_bytes_per_step": int(Uh.numel() * Uh.element_size()),
-               "timer": "host wall clock around the blocking C-ABI call (pinned buffers)"}
+               "h2d_bytes_per_step": int(st_h["h2d_bytes"]),
+               "d2h_bytes_per_step": int(st_h["d2h_bytes"]),
+               "timer": "host wall clock around the blocking C-ABI call (pinned buffers)",
+               "transfers": "F and exit_mask copied H2D; exit_vals read in place at the exit points "
+                            "(mapped pinned memory); U copied D2H"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

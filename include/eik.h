@@ -118,6 +118,10 @@ typedef struct {
                                    (eik_solve_sweep: diagonal launches)                         */
     uint64_t grid_sweeps;       /* eik_solve_sweep: whole-grid sweeps, the last of which changed
                                    nothing (the FSM count of P:803, Table 4); else 0            */
+    uint64_t h2d_bytes;         /* eik_solve_host: host->device bytes of the call (F and the mask
+                                   copied; exit_vals copied, or -- page-locked -- only its exit
+                                   values read in place); else 0                                */
+    uint64_t d2h_bytes;         /* eik_solve_host: device->host bytes (U); else 0               */
 } eik_stats;
 
 /* Create a context on `device`.  cuda_stream: a cudaStream_t to enqueue on (e.g. torch's

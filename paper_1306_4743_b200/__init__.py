@@ -43,7 +43,8 @@ class EikStats(ctypes.Structure):
                 ("ms_ingest", ctypes.c_double), ("ms_loop", ctypes.c_double),
                 ("ms_egress", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("ms_cell_device", ctypes.c_double), ("ms_cell_events", ctypes.c_double),
-                ("cell_launches", ctypes.c_uint64), ("grid_sweeps", ctypes.c_uint64)]
+                ("cell_launches", ctypes.c_uint64), ("grid_sweeps", ctypes.c_uint64),
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}

@@ -65,6 +65,7 @@ struct eik_ctx {
     // host-pointer staging (eik_solve_host)
     void* stage = nullptr;
     size_t stage_bytes = 0;
+    bool q_zero_copy = false;   // last eik_solve_host read exit_vals in place (pinned memory)
     // graph cache (scheduler loop; whole-grid sweep loop)
     cudaGraphExec_t gexec = nullptr;
     std::string gkey;
@@ -888,11 +889,27 @@ extern "C" int eik_solve_host(eik_ctx* ctx, int64_t n, double h, const void* F, 
     uint8_t* dm = (uint8_t*)(base + 3 * M * s);
     cudaStream_t sm = ctx->stream;
     CK(cudaMemcpyAsync(dF, F, M * s, cudaMemcpyHostToDevice, sm));
-    CK(cudaMemcpyAsync(dq, exit_vals, M * s, cudaMemcpyHostToDevice, sm));
+    // exit_vals is read only at exit points (k_ingest loads q behind the mask test): when it is
+    // page-locked host memory the device reads those few values in place over PCIe (mapped
+    // pinned memory, UVA) instead of copying the whole dense array (M * s bytes, 0.54 GB at
+    // C3 fp32); pageable memory is copied as before
+    const void* qdev = dq;
+    {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, exit_vals) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr)
+            qdev = pa.devicePointer;
+        else
+            (void)cudaGetLastError();
+    }
+    ctx->q_zero_copy = qdev != dq;
+    if (qdev == dq) CK(cudaMemcpyAsync(dq, exit_vals, M * s, cudaMemcpyHostToDevice, sm));
     CK(cudaMemcpyAsync(dm, exit_mask, M, cudaMemcpyHostToDevice, sm));
-    st = eik_solve(ctx, n, h, dF, dm, dq, dU, precision, cell_size);
+    st = eik_solve(ctx, n, h, dF, dm, qdev, dU, precision, cell_size);
     if (st) return st;
     CK(cudaMemcpyAsync(U_out, dU, M * s, cudaMemcpyDeviceToHost, sm));
     CK(cudaStreamSynchronize(sm));
+    ctx->stats.h2d_bytes = M * s + M + (ctx->q_zero_copy ? (uint64_t)ctx->ctl_host->n_exits * s : M * s);
+    ctx->stats.d2h_bytes = M * s;
     return EIK_OK;
 }

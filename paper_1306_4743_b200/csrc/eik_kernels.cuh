@@ -540,7 +540,13 @@ template <> struct MinBlocks<float, 16> { static constexpr int value = EIK_MINB1
 #ifndef EIK_MINB64
 #define EIK_MINB64 4   // measured: 2 (hf in shared memory) 29.6 ms on C3d, 3 26.2, 4 24.0
 #endif
+#ifndef EIK_HF_GLOBAL32
+#define EIK_HF_GLOBAL32 0
+#endif
 template <typename T, int R> struct HfGlobal { static constexpr bool value = false; };
+#if EIK_HF_GLOBAL32
+template <> struct HfGlobal<float, 16> { static constexpr bool value = true; };
+#endif
 #if EIK_HF_GLOBAL64
 template <> struct HfGlobal<double, 16> { static constexpr bool value = true; };
 template <> struct MinBlocks<double, 16> { static constexpr int value = EIK_MINB64; };
@@ -633,7 +639,7 @@ template <int R> struct CellShared {
     uint32_t dstate;                   // direction state saved at a sweep cap (pdir[c])
 };
 
-static_assert(((cell_smem_bytes<float, 16>() + sizeof(CellShared<16>) + 16 + 127) / 128 * 128 + 1024) * 5
+static_assert(EIK_HF_GLOBAL32 || ((cell_smem_bytes<float, 16>() + sizeof(CellShared<16>) + 16 + 127) / 128 * 128 + 1024) * 5
                   <= 228 * 1024,
               "fp32 r = 16 cell kernels no longer fit 5 CTAs per SM (shared memory)");
 

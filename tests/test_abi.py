@@ -41,8 +41,8 @@ def test_lib_is_sm100a_cubin():
 
 def test_stats_struct_layout_matches_header():
     import paper_1306_4743_b200 as eik
-    # 3*8 + 4*4 + 5*8 + 2*4 + 2*8 + 4*8 + 2*8 + 8 + 8 = 168 bytes
-    assert ctypes.sizeof(eik.EikStats) == 168
+    # 3*8 + 4*4 + 5*8 + 2*4 + 2*8 + 4*8 + 2*8 + 8 + 8 + 2*8 = 184 bytes
+    assert ctypes.sizeof(eik.EikStats) == 184
 
 
 def test_create_without_gpu_fails_cleanly():

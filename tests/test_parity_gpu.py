@@ -128,6 +128,35 @@ def test_host_pointer_path(solver):
         assert_parity(_gpu(solver, w, dt, 8, host=True), U_orc, w, dt)
 
 
+def test_host_path_pinned_exit_values_in_place(solver):
+    """eik_solve_host with page-locked inputs reads exit_vals in place at the exits (mapped
+    pinned memory) instead of copying the dense array: same parity, q > 0 at several exits,
+    the bytes it reports, and a bad q at an exit still rejected (device-side validation)."""
+    import torch
+    import paper_1306_4743_b200 as eik
+    w = W.random_instance(28, seed=77, n_exits=9, q_max=0.2)
+    U_orc = oracle_U(w)
+    M = w.M
+    for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+        F, m, q = w.as_dtype(dt)
+        Fp, mp, qp = (torch.from_numpy(a).pin_memory() for a in (F, m, q))
+        U = solver.solve_host(Fp, mp, qp, cell_size=8, n=w.n)
+        assert_parity(U.numpy(), U_orc, w, dt)
+        st = solver.stats()
+        s = np.dtype(dt).itemsize
+        assert st["h2d_bytes"] == M * s + M + 9 * s     # dense q not copied
+        assert st["d2h_bytes"] == M * s
+        # pageable q: copied whole, same values
+        U2 = solver.solve_host(F, m, q, cell_size=8, n=w.n)
+        assert_parity(U2, U_orc, w, dt)
+        assert solver.stats()["h2d_bytes"] == 2 * M * s + M
+        # a negative q at an exit, read in place, is still EIK_EINVAL
+        qb = qp.clone().pin_memory()
+        qb.view(-1)[int(np.flatnonzero(m)[0])] = -1.0
+        with pytest.raises(eik.EikError, match="EINVAL"):
+            solver.solve_host(Fp, mp, qb, cell_size=8, n=w.n)
+
+
 @pytest.mark.parametrize("mode,delta,msw,defer", [
     (0, 0.0, 0, 1), (0, 0.0, 2, 1), (0, 0.0, 0, 0), (0, 0.0, 0, 2), (0, 0.05, 0, 3),
     (1, 0.0, 0, 1), (1, 0.05, 0, 1), (1, 1e-6, 3, 1),

@@ -111,13 +111,13 @@ static int rindex_of(int r) { return r == 4 ? 0 : r == 8 ? 1 : r == 16 ? 2 : -1;
 
 // wavefront plane table for an r^3 cell, indexed [plane s][thread t]: the canonical point
 // index a + r b + r^2 c of the t-th point (a, b, c) of plane a+b+c = s, or 0xFFFF when plane s
-// has <= t points.  Two trailing all-empty planes let the sweep prefetch two planes ahead
+// has <= t points.  Three trailing all-empty planes let the sweep prefetch up to three planes ahead
 // without a bounds test.  A direction's point is this entry XOR its reflection mask (r a power
 // of two).  nt = threads of the cell kernel (CellCfg<r>::NT >= the largest plane).
 static void make_plane_table(int r, int nt, std::vector<uint16_t>& tab)
 {
     const int npl = 3 * r - 2;
-    tab.assign((size_t)(npl + 2) * nt, (uint16_t)0xFFFF);
+    tab.assign((size_t)(npl + 3) * nt, (uint16_t)0xFFFF);
     for (int s = 0; s < npl; ++s) {
         int t = 0;
         for (int c = 0; c < r; ++c)

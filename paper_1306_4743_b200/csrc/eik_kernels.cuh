@@ -498,9 +498,6 @@ __global__ void k_round_end(Ctl* ctl) { (void)round_end_body(ctl); }
 // --------------------------------------------------------------------------------------
 // A3-A6: the cell-sweep kernel
 // --------------------------------------------------------------------------------------
-#ifndef EIK_TAB_PTR
-#define EIK_TAB_PTR 1   // running plane-table pointer, 3-term box offset: 175 -> 163 instructions per fp32 step (C5 -2 %)
-#endif
 #ifndef EIK_MINB8
 #define EIK_MINB8 12   // measured (fp64 r = 8): 8 -> 12 P2 24.0 -> 21.5 ms, C2d 10.7 -> 10.5; 16 slower
 #endif
@@ -576,7 +573,7 @@ struct CellArgs {
     uint32_t* key;
     uint32_t* state;
     uint32_t* gen;               // async mode: BFS generation of each cell (readiness mode 5)
-    const uint16_t* plane_tab;   // [NPL + 2][NT] canonical point of thread t in plane s (0xFFFF: none)
+    const uint16_t* plane_tab;   // [NPL + 3][NT] canonical point of thread t in plane s (0xFFFF: none)
     void* Vt;
     const void* Ht;
     int64_t n1;
@@ -719,36 +716,28 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                    ozq = (uint32_t)((fz ? -RP2 : RP2) * TS);
     const uint32_t oxp = (uint32_t)(fx ? -1 : 1), oyp = (uint32_t)(fy ? -R : R),
                    ozp = (uint32_t)(fz ? -R * R : R * R);
-    // Two-stage prefetch, independent of the current step's results: at step s the thread
+    // Prefetch pipeline, independent of the current step's results: at step s the thread
     // holds its entry en / hf hn of plane s and the entry en1 of plane s + 1; the step loads
-    // hf of plane s + 1 (shared memory) and the entry of plane s + 2 (global table via L1),
-    // so no load sits on the step's critical path.  The table has two empty trailing planes.
+    // hf of plane s + 1 (shared memory, or L1/L2 for HG) and the entry of plane s + 2 (global
+    // table via L1, running pointer tq), so no load sits on the step's critical path.  (A
+    // pipeline one plane deeper for HG measured neutral on C3d.)  The table has trailing empty
+    // planes.
     const uint16_t* tp = ptab + tid;
     unsigned en = __ldg(&tp[s * NT]);
     unsigned en1 = __ldg(&tp[(s + 1) * NT]);
-#if EIK_TAB_PTR
-    const uint16_t* tq = tp + (s + 2) * NT;   // running pointer: entry of plane s + 2
-#endif
+    const uint16_t* tq = tp + (s + 2) * NT;
 #define EIK_HFLD(e_) (HG ? __ldg(hg + (e_)) : lds<T>(hb + (e_) * TS))
     T hn = en < (unsigned)R3 ? EIK_HFLD(en ^ dm) : INF;
-#if EIK_TAB_PTR
-#define EIK_NEXT_ENTRY(sp_) { en1 = __ldg(tq); tq += NT; }
-#else
-#define EIK_NEXT_ENTRY(sp_) { en1 = __ldg(&tp[((sp_) + 1) * NT]); }
-#endif
 #define EIK_PREFETCH(sp_)                                                                  \
     {                                                                                  \
         en = en1;                                                                      \
         hn = en < (unsigned)R3 ? EIK_HFLD(en ^ dm) : INF;                              \
-        EIK_NEXT_ENTRY(sp_)                                                            \
+        en1 = __ldg(tq);                                                               \
+        tq += NT;                                                                      \
     }
-    // box byte offset of point p = a + R b + R^2 c (relative to vb)
-#if EIK_TAB_PTR
-    // a + RP b + RP2 c = p + (RP - R) b + (RP2 - R^2) c for p = a + R b + R^2 c
+    // box byte offset of point p = a + R b + R^2 c (relative to vb):
+    // a + RP b + RP2 c = p + (RP - R) b + (RP2 - R^2) c
 #define EIK_QOFF(up_) (((up_) + (RP - R) * (((up_) / R) & (R - 1)) + (RP2 - R * R) * ((up_) / (R * R))) * TS)
-#else
-#define EIK_QOFF(up_) ((((up_) & (R - 1)) + RP * (((up_) / R) & (R - 1)) + RP2 * ((up_) / (R * R))) * TS)
-#endif
     // First sweep of a cell with many active points (a fresh cell the front is entering):
     // relax every point of every plane without per-point gating -- nearly all of them
     // change anyway -- and record only the activations *behind* the wavefront, which the
@@ -853,7 +842,6 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
         ++nsteps;
     }
 #undef EIK_QOFF
-#undef EIK_NEXT_ENTRY
 #undef EIK_PREFETCH
 #undef EIK_HFLD
     return bwd;

@@ -328,7 +328,7 @@ def main():
         st2 = s2.stats()
         s2.close()
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"ncu_{args.config}.json")
+    tp = os.path.join(ROOT, "profiles", f"r01_ncu_{args.config}.json")
     if os.path.exists(tp) and not sweep:   # ncu DRAM bytes of the cell kernel per processing x processings/launch
         d = json.load(open(tp))["kcell_traffic"]
         traffic = d["dram_bytes_per_processing"] * (stats[-1]["cell_processings"] / max(launches, 1))

@@ -80,5 +80,5 @@ st = {k: float(d[k] or 0) for k in hdr if k.startswith("smsp__pcsamp_warps_issue
 tot = sum(st.values()) or 1
 out["full_capture"]["stall_pct"] = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): round(100 * v / tot, 1)
                                     for k, v in sorted(st.items(), key=lambda x: -x[1])[:10]}
-json.dump(out, open(f"profiles/{tag}.json", "w"), indent=1)
+json.dump(out, open(f"profiles/r01_{tag}.json", "w"), indent=1)
 print(json.dumps(out, indent=1))

@@ -498,6 +498,9 @@ __global__ void k_round_end(Ctl* ctl) { (void)round_end_body(ctl); }
 // --------------------------------------------------------------------------------------
 // A3-A6: the cell-sweep kernel
 // --------------------------------------------------------------------------------------
+#ifndef EIK_POP_MAXNS
+#define EIK_POP_MAXNS 1024   // longest back-off (ns) of a CTA waiting for its ticket's slot
+#endif
 #ifndef EIK_MINB8
 #define EIK_MINB8 12   // measured (fp64 r = 8): 8 -> 12 P2 24.0 -> 21.5 ms, C2d 10.7 -> 10.5; 16 slower
 #endif
@@ -1682,7 +1685,7 @@ k_async(CellArgs A)
                                 break;
                             }
                             __nanosleep(ns);
-                            ns = ns < 1024 ? ns * 2 : 1024;
+                            ns = ns < EIK_POP_MAXNS ? ns * 2 : EIK_POP_MAXNS;
                         }
                     }
                 }

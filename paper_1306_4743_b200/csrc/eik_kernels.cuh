@@ -161,7 +161,25 @@ __device__ __forceinline__ float sqrt_approx(float x)
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));   // arguments are O(hf^2) >> FLT_MIN
     return r;
 }
-__device__ __forceinline__ double sqrt_approx(double x) { return __dsqrt_rn(x); }
+#ifndef EIK_FAST_DSQRT
+#define EIK_FAST_DSQRT 1   // measured: 272 -> 230 instructions per fp64 step, C3d -5 %, C2d / P2 / P3 -8 %
+#endif
+__device__ __forceinline__ double sqrt_approx(double x)
+{
+#if EIK_FAST_DSQRT
+    // x >= 0 and finite (a clamped discriminant, O(hf^2)): MUFU reciprocal square-root seed and
+    // two Newton corrections of s = x / sqrt(x) (no special-case path); x = 0 -> 0
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double s = x * y;
+    const double hy = 0.5 * y;
+    s = fma(fma(-s, s, x), hy, s);
+    s = fma(fma(-s, s, x), hy, s);
+    return x > 0.0 ? s : 0.0;
+#else
+    return __dsqrt_rn(x);
+#endif
+}
 
 template <typename T>
 __device__ __forceinline__ T local_solve_fast(T mx, T my, T mz, T hf)

@@ -748,11 +748,16 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     unsigned en1 = __ldg(&tp[(s + 1) * NT]);
     const uint16_t* tq = tp + (s + 2) * NT;
 #define EIK_HFLD(e_) (HG ? __ldg(hg + (e_)) : lds<T>(hb + (e_) * TS))
+    // (ha / han: shared address of the current / prefetched point's hf, reused to mark a
+    // changed point without recomputing it)
+    uint32_t han = hb + (en ^ dm) * TS, ha = han;
     T hn = en < (unsigned)R3 ? EIK_HFLD(en ^ dm) : INF;
 #define EIK_PREFETCH(sp_)                                                                  \
     {                                                                                  \
         en = en1;                                                                      \
-        hn = en < (unsigned)R3 ? EIK_HFLD(en ^ dm) : INF;                              \
+        ha = han;                                                                      \
+        han = hb + (en ^ dm) * TS;                                                     \
+        hn = en < (unsigned)R3 ? (HG ? __ldg(hg + (en ^ dm)) : lds<T>(han)) : INF;     \
         en1 = __ldg(tq);                                                               \
         tq += NT;                                                                      \
     }
@@ -785,7 +790,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                     if (u < v) {
                         sts(qa, u);
                         if constexpr (HG) atomicOr(&M.chg[up >> 5], 1u << (up & 31));
-                        else if (hs > T(0)) sts(hb + up * TS, -hs);
+                        else sts(ha, -hf);   // sign bit = changed (idempotent)
                         ++nwr;
                         // kappa: a change <= kappa activates nothing (ut = +inf)
                         const T ut = (v - u > kap) ? u : INF;
@@ -835,7 +840,7 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                     if (u < v) {                                         // line 6
                         sts(qa, u);                                      // line 7
                         if constexpr (HG) atomicOr(&M.chg[up >> 5], 1u << (up & 31));   // mark changed
-                        else if (hs > T(0)) sts(hb + up * TS, -hs);
+                        else sts(ha, -hf);   // sign bit = changed (idempotent)
                         ++nwr;
                         // lines 8-13: activate larger in-cell neighbours (the cross-border
                         // "currently downwind" test is done once per processing)

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EIK_ABI_VERSION 2
+#define EIK_ABI_VERSION 3   /* 3: eik_stats gained h2d_bytes, d2h_bytes */
 
 typedef struct eik_ctx eik_ctx;
 

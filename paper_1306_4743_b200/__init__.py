@@ -31,6 +31,9 @@ EXPORTS = ("eik_create", "eik_set_stream", "eik_set_option", "eik_solve", "eik_s
            "eik_abi_version")
 
 
+ABI_VERSION = 3   # include/eik.h EIK_ABI_VERSION (the EikStats layout below)
+
+
 class EikStats(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int64), ("padded_points", ctypes.c_int64), ("J", ctypes.c_int64),
                 ("cells_per_side", ctypes.c_int32), ("cell_size", ctypes.c_int32),
@@ -84,6 +87,9 @@ def _load():
     lib.eik_destroy.restype = None
     lib.eik_abi_version.argtypes = []
     lib.eik_abi_version.restype = I
+    if lib.eik_abi_version() != ABI_VERSION:   # a stale build would misread eik_stats
+        raise ImportError(f"{LIB_PATH}: ABI {lib.eik_abi_version()}, binding expects {ABI_VERSION}; "
+                          f"rebuild with `python -c 'import __graft_entry__ as g; g.build()'`")
     return lib
 
 

@@ -236,3 +236,88 @@ def test_residual_ratio_checker():
     V[10, 11, 12] += 1e-4
     rb, at = oracle.residual_ratio(n, w.F, w.exit_mask, V, 2.0 ** -24)
     assert rb > 10.0
+
+
+# ---- negative pins of the invariant checker (orc_check): each detector must fire on a
+# solution broken in exactly the way it is meant to catch (VERDICT r1 "What's missing" 3).
+# The checker evaluates Eq. (2)'s residual, the discrete Lipschitz bound implied
+# by the one-sided update (U_p <= U_r + hf_p for every axis neighbour r, Eq. (2) with one
+# finite minimum), causality (a finite non-exit value has a strictly smaller
+# neighbour), R11 (F = 0 non-exit points stay +inf) and reachability (U finite iff some
+# neighbour is finite, C.1).  The correct FMM fixed point must pass every detector.
+
+def _pocket_instance():
+    n = 12
+    F = np.ones((n + 1,) * 3)
+    F[3:9, 3:9, 3:9] = 0.0          # closed F = 0 shell ...
+    F[4:8, 4:8, 4:8] = 1.0          # ... around an F = 1 pocket (unreachable: +inf)
+    mask = np.zeros(F.shape, np.uint8)
+    mask[0, 0, 0] = 1
+    q = np.zeros(F.shape)
+    return n, F, mask, q
+
+
+def _clean(n, F, mask, q):
+    U = oracle.fmm(n, F, mask, q)
+    st = oracle.check(n, F, mask, U)
+    assert st["res_max"] < 1e-12 and st["lip_max"] <= 1e-12
+    assert st["causal_bad"] == 0 and st["f0_finite"] == 0 and st["inf_bad"] == 0
+    return U
+
+
+def test_check_lipschitz_detector_fires():
+    n, F, mask, q = _pocket_instance()
+    U = _clean(n, F, mask, q)
+    h = 1.0 / n
+    k, j, i = 10, 11, 2                 # reachable, outside the shell, interior of the grid
+    nb = [U[k, j, i - 1], U[k, j, i + 1], U[k, j - 1, i], U[k, j + 1, i], U[k - 1, j, i], U[k + 1, j, i]]
+    V = U.copy()
+    V[k, j, i] = min(nb) + 2.0 * h      # raised a full hf above min neighbour + hf (F = 1)
+    st = oracle.check(n, F, mask, V)
+    assert st["lip_max"] >= 1.0 - 1e-12  # (U_p - U_r - hf) / hf = 1 for the smallest neighbour
+    assert st["causal_bad"] == 0 and st["f0_finite"] == 0 and st["inf_bad"] == 0
+
+
+def test_check_causal_detector_fires():
+    n, F, mask, q = _pocket_instance()
+    U = _clean(n, F, mask, q)
+    h = 1.0 / n
+    k, j, i = 10, 11, 2
+    nb = [U[k, j, i - 1], U[k, j, i + 1], U[k, j - 1, i], U[k, j + 1, i], U[k - 1, j, i], U[k + 1, j, i]]
+    V = U.copy()
+    V[k, j, i] = min(nb) - 0.25 * h     # an isolated local minimum: no strictly smaller neighbour
+    st = oracle.check(n, F, mask, V)
+    assert st["causal_bad"] == 1
+    assert st["res_max"] > 0.5          # Eq. (2) is violated there too (sum of max(.,0)^2 = 0)
+    assert st["f0_finite"] == 0 and st["inf_bad"] == 0
+
+
+def test_check_f0_detector_fires():
+    n, F, mask, q = _pocket_instance()
+    U = _clean(n, F, mask, q)
+    V = U.copy()
+    assert F[3, 3, 3] == 0.0 and not mask[3, 3, 3]
+    V[3, 3, 3] = 0.5                    # a finite value on a corner of the F = 0 shell (R11);
+                                        # no pocket point touches it, so nothing else fires
+    st = oracle.check(n, F, mask, V)
+    assert st["f0_finite"] == 1
+    assert st["causal_bad"] == 0 and st["inf_bad"] == 0
+
+
+def test_check_inf_detector_fires_both_ways():
+    n, F, mask, q = _pocket_instance()
+    U = _clean(n, F, mask, q)
+    # (a) a finite value inside the unreachable pocket: all of its neighbours are +inf
+    V = U.copy()
+    assert np.isinf(V[5, 5, 5])
+    V[5, 5, 5] = 0.7
+    st = oracle.check(n, F, mask, V)
+    # the point itself (finite, every neighbour +inf) and its six pocket neighbours (+inf next
+    # to a now finite neighbour)
+    assert st["inf_bad"] == 7 and st["f0_finite"] == 0
+    # (b) +inf at a reachable point that has a finite neighbour
+    V = U.copy()
+    V[10, 11, 2] = np.inf
+    st = oracle.check(n, F, mask, V)
+    assert st["inf_bad"] == 1
+    assert st["f0_finite"] == 0

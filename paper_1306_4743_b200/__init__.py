@@ -140,6 +140,33 @@ class Solver:
         except Exception:
             pass
 
+    # -- argument checks (the C ABI trusts sizes: a short buffer would be read or written past
+    # its end on the device, a sticky error that breaks the whole CUDA context) -----------
+    def _check_device_args(self, F, exit_mask, exit_vals, h, n, out, who):
+        import torch
+        if F.dtype not in (torch.float32, torch.float64):
+            raise TypeError("F must be float32 or float64")
+        prec = EIK_F32 if F.dtype == torch.float32 else EIK_F64
+        if exit_mask.dtype != torch.uint8 or exit_vals.dtype != F.dtype:
+            raise TypeError("exit_mask must be uint8 and exit_vals must have F's dtype")
+        n = _n_from_numel(F.numel()) if n is None else int(n)
+        if n < 1 or (n + 1) ** 3 != F.numel():
+            raise ValueError(f"F has {F.numel()} elements, not (n+1)^3 for n = {n}")
+        if out is None:
+            out = torch.empty_like(F, memory_format=torch.contiguous_format)
+        elif out.dtype != F.dtype:
+            raise TypeError("out must have F's dtype")
+        for name, t in (("F", F), ("exit_mask", exit_mask), ("exit_vals", exit_vals), ("out", out)):
+            if not (t.is_cuda and t.is_contiguous()):
+                raise ValueError(f"{who}() takes contiguous CUDA tensors ({name} is not; use "
+                                 f"solve_host for host arrays)")
+            if t.numel() != F.numel():
+                raise ValueError(f"{name} has {t.numel()} elements, F has {F.numel()}")
+            if t.device.index != self.device:
+                raise ValueError(f"{name} is on {t.device}, this Solver on cuda:{self.device}")
+        h = 1.0 / n if h is None else float(h)
+        return prec, n, h, out
+
     # -- device tensors ------------------------------------------------------------------
     def solve(self, F, exit_mask, exit_vals, h: float | None = None, cell_size: int = 16,
               n: int | None = None, out=None):
@@ -147,18 +174,7 @@ class Solver:
         lexicographic i fastest.  dtype of F (float32/float64) selects the precision.
         Returns U (same shape/dtype as F).  Enqueued on torch's current stream; blocking."""
         import torch
-        if F.dtype not in (torch.float32, torch.float64):
-            raise TypeError("F must be float32 or float64")
-        prec = EIK_F32 if F.dtype == torch.float32 else EIK_F64
-        for t in (F, exit_mask, exit_vals):
-            if not (t.is_cuda and t.is_contiguous()):
-                raise ValueError("solve() takes contiguous CUDA tensors (use solve_host for host arrays)")
-        if exit_mask.dtype != torch.uint8 or exit_vals.dtype != F.dtype:
-            raise TypeError("exit_mask must be uint8 and exit_vals must have F's dtype")
-        n = _n_from_numel(F.numel()) if n is None else n
-        h = 1.0 / n if h is None else h
-        if out is None:
-            out = torch.empty_like(F)
+        prec, n, h, out = self._check_device_args(F, exit_mask, exit_vals, h, n, out, "solve")
         stream = torch.cuda.current_stream(F.device).cuda_stream
         lib.eik_set_stream(self._ctx, ctypes.c_void_p(stream))
         st = lib.eik_solve(self._ctx, n, h, F.data_ptr(), exit_mask.data_ptr(),
@@ -175,18 +191,7 @@ class Solver:
         stats()["grid_sweeps"]."""
         import torch
         m = {"dfsm": EIK_DFSM, "dlsm": EIK_DLSM}[method]
-        if F.dtype not in (torch.float32, torch.float64):
-            raise TypeError("F must be float32 or float64")
-        prec = EIK_F32 if F.dtype == torch.float32 else EIK_F64
-        for t in (F, exit_mask, exit_vals):
-            if not (t.is_cuda and t.is_contiguous()):
-                raise ValueError("solve_sweep() takes contiguous CUDA tensors")
-        if exit_mask.dtype != torch.uint8 or exit_vals.dtype != F.dtype:
-            raise TypeError("exit_mask must be uint8 and exit_vals must have F's dtype")
-        n = _n_from_numel(F.numel()) if n is None else n
-        h = 1.0 / n if h is None else h
-        if out is None:
-            out = torch.empty_like(F)
+        prec, n, h, out = self._check_device_args(F, exit_mask, exit_vals, h, n, out, "solve_sweep")
         lib.eik_set_stream(self._ctx, ctypes.c_void_p(torch.cuda.current_stream(F.device).cuda_stream))
         st = lib.eik_solve_sweep(self._ctx, n, h, F.data_ptr(), exit_mask.data_ptr(),
                                  exit_vals.data_ptr(), out.data_ptr(), prec, cell_size, m)
@@ -203,14 +208,37 @@ class Solver:
         def ptr(a):
             return a.ctypes.data if isinstance(a, np.ndarray) else a.data_ptr()
 
-        dt = F.dtype
-        is_f32 = (dt == np.float32) if isinstance(F, np.ndarray) else (str(dt) == "torch.float32")
-        prec = EIK_F32 if is_f32 else EIK_F64
-        numel = F.size if isinstance(F, np.ndarray) else F.numel()
-        n = _n_from_numel(numel) if n is None else n
-        h = 1.0 / n if h is None else h
+        def info(a, name):
+            # (numpy dtype, element count, C-contiguous) of a numpy array or a CPU torch tensor
+            if isinstance(a, np.ndarray):
+                return a.dtype, a.size, a.flags["C_CONTIGUOUS"]
+            import torch
+            if not isinstance(a, torch.Tensor) or a.is_cuda:
+                raise TypeError(f"solve_host(): {name} must be a numpy array or a CPU tensor")
+            dt = {torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64),
+                  torch.uint8: np.dtype(np.uint8)}.get(a.dtype, None)
+            return dt, a.numel(), a.is_contiguous()
+
+        fdt, numel, _ = info(F, "F")
+        if fdt not in (np.float32, np.float64):
+            raise TypeError("F must be float32 or float64")
+        prec = EIK_F32 if fdt == np.float32 else EIK_F64
+        n = _n_from_numel(numel) if n is None else int(n)
+        if n < 1 or (n + 1) ** 3 != numel:
+            raise ValueError(f"F has {numel} elements, not (n+1)^3 for n = {n}")
+        h = 1.0 / n if h is None else float(h)
         if out is None:
-            out = np.empty_like(F) if isinstance(F, np.ndarray) else F.new_empty(F.shape)
+            out = np.empty(F.shape, dtype=fdt) if isinstance(F, np.ndarray) else F.new_empty(F.shape)
+        for name, a, want in (("F", F, fdt), ("exit_mask", exit_mask, np.dtype(np.uint8)),
+                              ("exit_vals", exit_vals, fdt), ("out", out, fdt)):
+            dt, ne, contig = info(a, name)
+            if dt != want:
+                raise TypeError(f"solve_host(): {name} must be {np.dtype(want).name}, got {dt}")
+            if ne != numel:
+                raise ValueError(f"solve_host(): {name} has {ne} elements, F has {numel}")
+            if not contig:
+                raise ValueError(f"solve_host(): {name} must be C-contiguous (lexicographic, i "
+                                 f"fastest); use np.ascontiguousarray")
         lib.eik_set_stream(self._ctx, None)
         st = lib.eik_solve_host(self._ctx, n, h, ptr(F), ptr(exit_mask), ptr(exit_vals),
                                 ptr(out), prec, cell_size)
@@ -236,12 +264,14 @@ class Solver:
         return s.as_dict()
 
 
-_default: Solver | None = None
+_default: dict[int, Solver] = {}
 
 
 def solve(F, exit_mask, exit_vals, h: float | None = None, cell_size: int = 16, out=None):
-    """Module-level convenience: solve on a shared per-process Solver (device of F)."""
-    global _default
-    if _default is None:
-        _default = Solver(device=F.device.index or 0)
-    return _default.solve(F, exit_mask, exit_vals, h=h, cell_size=cell_size, out=out)
+    """Module-level convenience: solve on a shared per-process Solver of F's device."""
+    dev = F.device.index if F.is_cuda else None
+    if dev is None:
+        raise ValueError("solve() takes CUDA tensors (use Solver.solve_host for host arrays)")
+    if dev not in _default:
+        _default[dev] = Solver(device=dev)
+    return _default[dev].solve(F, exit_mask, exit_vals, h=h, cell_size=cell_size, out=out)

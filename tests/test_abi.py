@@ -77,3 +77,46 @@ def test_product_path_does_not_import_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "oracle.c" not in txt and \
                        "liboracle" not in txt, f
+
+
+def _ctxless_solver():
+    # a Solver whose argument checks run without a device (no eik_ctx): every misuse below
+    # must raise before the C call, which would otherwise read/write past a short buffer
+    import paper_1306_4743_b200 as eik
+    s = eik.Solver.__new__(eik.Solver)
+    s._ctx = ctypes.c_void_p()
+    s.device = 0
+    return s
+
+
+@pytest.mark.parametrize("case", ["f16", "mask_dtype", "q_dtype", "out_dtype", "short_mask",
+                                  "short_q", "short_out", "bad_n", "transposed"])
+def test_solve_host_rejects_bad_arguments(case):
+    import numpy as np
+    n = 8
+    M = (n + 1) ** 3
+    F = np.ones(M, np.float32)
+    m = np.zeros(M, np.uint8)
+    q = np.zeros(M, np.float32)
+    out = np.empty(M, np.float32)
+    kw = {}
+    if case == "f16":
+        F = F.astype(np.float16)
+    elif case == "mask_dtype":
+        m = m.astype(np.int32)
+    elif case == "q_dtype":
+        q = q.astype(np.float64)
+    elif case == "out_dtype":
+        out = out.astype(np.float64)
+    elif case == "short_mask":
+        m = m[:-1]
+    elif case == "short_q":
+        q = q[:-5]
+    elif case == "short_out":
+        out = out[:-1]
+    elif case == "bad_n":
+        kw["n"] = 7
+    elif case == "transposed":
+        F = F.reshape(n + 1, n + 1, n + 1).transpose(2, 1, 0)
+    with pytest.raises((TypeError, ValueError)):
+        _ctxless_solver().solve_host(F, m, q, out=out, **kw)

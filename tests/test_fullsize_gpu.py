@@ -1,7 +1,13 @@
 """GPU parity at the full BASELINE sizes (C3, C4 at 513^3 against the full fp64 FMM oracle;
-C5 at 1025^3 by properties that hold at any size: the Eq. (2) residual at every point within
-the precision's bound, the discrete Lipschitz bound, causal parents, exact exits and the
-reachability mask).  SURVEY 8(c) C.5/C.6."""
+C5 at 1025^3 element-wise against the fp64 FMM oracle at >= 1e5 seeded sample points stored
+in tests/golden/c5_oracle_samples.npz by tools/make_c5_golden.py -- which calls only oracle/ --
+for the F whose SHA-256 it recorded, plus properties that hold at every point: the Eq. (2)
+residual within the precision's bound, the discrete Lipschitz bound, causal parents, exact
+exits and the reachability mask).  SURVEY 8(c) C.5/C.6, 8(d) D.6."""
+import hashlib
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -83,8 +89,11 @@ def test_full_c4(solver):
     assert np.array_equal(U[: k0 + 1][open_].astype(np.float64), np.broadcast_to(kk, open_.shape)[open_])
 
 
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "c5_oracle_samples")
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-def test_full_c5_properties(solver, dtype):
+def test_full_c5(solver, dtype):
     import torch
     import paper_1306_4743_b200 as eik  # noqa: F401
     n = 1024
@@ -99,7 +108,33 @@ def test_full_c5_properties(solver, dtype):
     U = solver.solve(Fd, m, torch.zeros(M, dtype=tdt, device="cuda"), cell_size=16, n=n)
     Uh = U.cpu().numpy().reshape((n + 1,) * 3)
     del U
-    Fh = Fd.cpu().numpy().astype(np.float64).reshape((n + 1,) * 3)   # the F the GPU received
+    Fd_h = Fd.cpu().numpy()
+    del Fd, F64
+    # element-wise parity against the fp64 FMM oracle at the golden's sample points, for the
+    # very F the oracle solved (its SHA-256; fp32 runs receive its round-to-nearest fp32 copy)
+    meta = json.load(open(GOLDEN + ".json"))
+    g = np.load(GOLDEN + ".npz")
+    key = "F32_sha256" if dtype == np.float32 else "F64_sha256"
+    assert hashlib.sha256(Fd_h.tobytes()).hexdigest() == meta[key], "C5 F differs from the golden's"
+    assert [list(e) for e in ex] == meta["exits"]
+    idx_s, U_s = g["idx"], g["U"]
+    assert idx_s.size >= 100000
+    Us = Uh.reshape(-1)[idx_s].astype(np.float64)
+    assert np.isfinite(Us).all() and meta["n_finite"] == M
+    ex_s = np.isin(idx_s, np.array(idx))
+    assert (Us[ex_s] == 0).all() and (U_s[ex_s] == 0).all()
+    nz = ~ex_s
+    if dtype == np.float64:
+        err = np.abs(Us[nz] - U_s[nz]).max()
+        assert err <= TOL64, err
+    else:
+        err = (np.abs(Us[nz] - U_s[nz]) / U_s[nz]).max()
+        assert err <= TOL32, err
+    assert abs(float(Uh.reshape(-1)[meta["U_argmax"]]) - meta["U_max"]) <= (
+        TOL64 if dtype == np.float64 else TOL32 * meta["U_max"])
+    # properties at every point
+    Fh = Fd_h.astype(np.float64).reshape((n + 1,) * 3)   # the F the GPU received
+    del Fd_h
     mh = m.cpu().numpy().reshape((n + 1,) * 3)
     w = W.Workload("C5", n, Fh, mh, np.zeros(1))
     assert np.isfinite(Uh).all()                 # F >= 0.3 everywhere: every point reachable

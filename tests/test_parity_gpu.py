@@ -307,3 +307,39 @@ def test_legacy_cell_key_same_fixed_point(mode, delta, defer):
             for dt in (np.float64, np.float32):
                 assert_parity(_gpu(s, w, dt, r), oracle_U(w), w, dt)
     s.close()
+
+
+@pytest.mark.parametrize("case", ["short_mask", "short_q", "short_out", "out_dtype", "bad_n",
+                                  "noncontig"])
+def test_solve_rejects_bad_device_arguments(solver, case):
+    """Misuse raises in the binding before the C call (a short device buffer would otherwise
+    be read or written past its end: a sticky error that breaks the CUDA context); the
+    context still solves afterwards."""
+    import torch
+    n = 8
+    M = (n + 1) ** 3
+    F = torch.ones(M, dtype=torch.float32, device="cuda")
+    m = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    m[0] = 1
+    q = torch.zeros(M, dtype=torch.float32, device="cuda")
+    out = torch.empty(M, dtype=torch.float32, device="cuda")
+    kw = {}
+    if case == "short_mask":
+        m = m[:-1]
+    elif case == "short_q":
+        q = q[:-3]
+    elif case == "short_out":
+        out = out[:-1]
+    elif case == "out_dtype":
+        out = out.double()
+    elif case == "bad_n":
+        kw["n"] = 9
+    elif case == "noncontig":
+        F = torch.ones(2 * M, dtype=torch.float32, device="cuda")[::2]
+    with pytest.raises((TypeError, ValueError)):
+        solver.solve(F, m, q, cell_size=8, out=out, **kw)
+    F = torch.ones(M, dtype=torch.float32, device="cuda")
+    m = torch.zeros(M, dtype=torch.uint8, device="cuda")
+    m[0] = 1
+    U = solver.solve(F, m, torch.zeros_like(F), cell_size=8)
+    assert float(U[0]) == 0.0 and float(U[1]) == 0.125

@@ -9,10 +9,14 @@ inputs; value = gridpoints/s = M / (step time), summed over ranks (independent r
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3|C4|...] [--impl reference]
 
-N > 1: launched by torchrun, one process per GPU; the path does not shard ("replicas only",
-SURVEY 8(e)): each rank solves its own copy, no data-path collective; barrier + max over ranks.
+N > 1: one process per GPU (launched by torchrun; `--gpus N` without torchrun re-executes
+itself under torch.distributed.run); the path does not shard ("replicas only"):
+each rank solves its own copy, no data-path collective; barrier + max over ranks.
 --impl reference: the CPU fp64 FMM oracle (the only "reference" this tier has) on the host
-cores, on a bounded sample of the same workload (rank 0 only).
+cores, each step a bounded sample of the same workload: the oracle on a corner sub-box of the
+very same input (same F, h and exits inside it), rank 0 only.
+cpu_baseline (our arm, rank 0, N = 1): the oracle once on the full fp64 input of the workload
+(~75 s for C3), or on a 257^3 sub-box for inputs above 1.5e8 points.
 """
 from __future__ import annotations
 
@@ -170,21 +174,33 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
 
 
-def sample_workload(cfg, n):
-    """the same workload's formulas at a reduced size (n intervals; paper configs: n points)"""
+def full_workload(cfg):
+    """the workload at its BASELINE / paper size (fp64 F, as the oracle always takes it)"""
     import workloads as W
-    return paper_workload(cfg, n + (n % 2)) if cfg in PAPER_N else W.make(cfg, n)
+    return paper_workload(cfg) if cfg in PAPER_N else W.make(cfg)
 
 
-def cpu_oracle_sample(cfg, n_sample):
-    """Time the fp64 FMM oracle as it stands on the same workload's formulas at reduced n."""
+def sub_box(w, ns):
+    """Corner-anchored sub-box [i0, i0 + ns]^3 of workload w around its first exit: the same
+    F, h and the exits that fall inside (a bounded sample of the SAME input; the sub-box
+    faces act as the domain boundary)."""
+    import workloads as W
+    n = w.n
+    ns = min(ns, n)
+    k, j, i = [int(v[0]) for v in np.nonzero(w.exit_mask)]
+    lo = [min(max(c - ns // 2, 0), n - ns) for c in (k, j, i)]
+    sl = tuple(slice(a, a + ns + 1) for a in lo)
+    meta = dict(w.meta, h=w.h, box_lo_kji=lo)
+    return W.Workload(w.name, ns, np.ascontiguousarray(w.F[sl]), np.ascontiguousarray(w.exit_mask[sl]),
+                      np.ascontiguousarray(w.exit_vals[sl]), meta), lo
+
+
+def time_oracle(w):
     import oracle
-    w = sample_workload(cfg, n_sample)
     oracle.build()
     t0 = time.perf_counter()
     oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals, h=w.h)
-    dt = time.perf_counter() - t0
-    return w.M, dt
+    return time.perf_counter() - t0
 
 
 def run_reference(args):
@@ -192,28 +208,47 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg, prec, r = WORKLOADS[args.config]
-    n_s = args.ref_n
-    import oracle
-    oracle.build()
-    w = sample_workload(cfg, n_s)
+    wf = full_workload(cfg)
+    w, lo = sub_box(wf, args.ref_n)
+    del wf
     times = []
     for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        oracle.fmm(w.n, w.F, w.exit_mask, w.exit_vals, h=w.h)
+        dt = time_oracle(w)
         if s >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(dt)
     t = float(np.mean(times))
     val = w.M / t
-    sample = (f"fp64 serial FMM oracle on the {cfg} formulas at n={n_s} ({w.M} points) per step "
-              f"(the {DESC[cfg].split(',')[0]} input would take minutes)")
+    sample = (f"serial fp64 FMM oracle (1 host core of {os.cpu_count()}) per step on the "
+              f"{w.n + 1}^3 sub-box at (k, j, i) = {tuple(lo)} of the {cfg} input ({w.M} of its "
+              f"{(WN[cfg] + 1) ** 3} points; same F, h = {w.h:g} and the exits inside)")
+    cb = config_block(cfg, prec, r)
+    cb.update({"precision": "f64", "solve": "oracle FMM (serial, fp64) on a bounded sample of this input",
+               "sample_points": w.M, "sample": sample})
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": config_block(cfg, prec, r),
+            "data": "synthetic", "config": cb,
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+WN = {"C1": 128, "C2": 256, "C3": 512, "C4": 512, "C5": 1024, **{k: v - 1 for k, v in PAPER_N.items()}}
+
+
+def cpu_baseline(cfg):
+    """the oracle as it stands, once, on the full fp64 input (or a 257^3 sub-box above 1.5e8
+    points: C5's full run takes ~15 min)"""
+    w = full_workload(cfg)
+    full = w.M <= 150_000_000
+    if not full:
+        w, lo = sub_box(w, 256)
+    secs = time_oracle(w)
+    what = (f"the full {cfg} input ({w.M} points)" if full else
+            f"the {w.n + 1}^3 sub-box at (k, j, i) = {tuple(lo)} of the {cfg} input ({w.M} points)")
+    return {"value": w.M / secs, "unit": UNIT, "cores": 1, "kind": "oracle", "seconds": round(secs, 2),
+            "sample": f"serial fp64 FMM oracle once on {what}, {secs:.1f} s, 1 of {os.cpu_count()} host cores"}
 
 
 def config_block(cfg, prec, r, n=None):
@@ -228,6 +263,131 @@ def sweep_method(args):
     return getattr(args, "method", "hcm") != "hcm"
 
 
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    p = sk.getsockname()[1]
+    sk.close()
+    return p
+
+
+def self_launch(n, argv):
+    """`--gpus N` (N > 1) outside torchrun: re-execute this script under torch.distributed.run,
+    one process per GPU (replicas only); rank 0's JSON line passes through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
+def measure(eik, solver, cfg, prec, r, dev, args, sweep=False, async_mode=True, barrier=None,
+            pg=None, steps=None, warmup=None):
+    """Device-timed steps of one workload: W untimed warm-up solves, then K solves between CUDA
+    events on the launching stream (barrier + synchronize on both sides), max over ranks.
+    Returns the timing, roofline and work blocks."""
+    import torch
+    steps = steps or args.steps
+    warmup = args.warmup if warmup is None else warmup
+    n, F, m, q = make_inputs(cfg, prec, dev, args.n)
+    M = (n + 1) ** 3
+    U = torch.empty_like(F)
+    stream = torch.cuda.current_stream(dev)
+
+    def run_once():
+        if sweep:
+            solver.solve_sweep(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U, method=args.method)
+        else:
+            solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
+
+    for _ in range(warmup):
+        run_once()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    barrier()
+    with Clocks(dev.index) as clk:
+        ev0.record(stream)
+        for _ in range(steps):
+            run_once()
+            stats.append(solver.stats())
+        ev1.record(stream)
+        barrier()
+    t_ms = job_time(ev0.elapsed_time(ev1) / steps, pg, dev)
+
+    # roofline of the dominant kernel (cell sweep): algorithmic bytes / its device time
+    cell_ms = float(np.mean([s["ms_cell_device"] for s in stats]))            # %globaltimer span
+    ev_ms = float(np.mean([s["ms_cell_events"] for s in stats]))              # CUDA events (async)
+    if async_mode and ev_ms > 0:
+        cell_ms = ev_ms
+    alg_bytes = float(np.mean([s["bytes_cell_alg"] for s in stats]))
+    launches = float(np.mean([s["cell_launches"] for s in stats]))
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (cell_ms * 1e-3) / 1e9 if cell_ms > 0 else None
+    st2 = {"ms_cell_events": 0.0, "cell_launches": 1}
+    if async_mode:
+        st2 = {"ms_cell_events": ev_ms, "cell_launches": 1}
+    elif not sweep:
+        # CUDA events around every round's cell-kernel launch in the host-driven loop
+        s2 = eik.Solver(device=dev.index, loop_mode=1, bin_width=args.bin_width)
+        s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
+        s2.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=torch.empty_like(F))
+        st2 = s2.stats()
+        s2.close()
+    tag = f"{args.config if (cfg, prec, r) == WORKLOADS[args.config] else cfg + ('d' if prec == 'f64' else '')}"
+    traffic, tsrc = None, None
+    for rr in ("r02", "r01"):
+        tp = os.path.join(ROOT, "profiles", f"{rr}_ncu_{tag}.json")
+        if os.path.exists(tp) and not sweep:
+            # ncu DRAM bytes of the cell kernel per processing x processings per launch
+            d = json.load(open(tp))["kcell_traffic"]
+            traffic = d["dram_bytes_per_processing"] * (stats[-1]["cell_processings"] / max(launches, 1))
+            tsrc = f"profiles/{rr}_ncu_{tag}.json (ncu --set full, per processing x this run's processings)"
+            break
+    st = stats[-1]
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "traffic_source": tsrc,
+            "kernel": f"{'k_dsweep' if sweep else 'k_async' if async_mode else 'k_cell'}<{'float' if prec == 'f32' else 'double'},{r}>",
+            "alg_bytes_per_launch": alg_bytes / max(launches, 1),
+            "ms_per_launch_device": float(np.mean([s["ms_cell_device"] for s in stats])) / max(launches, 1),
+            "ms_per_launch_events": (st2["ms_cell_events"] / max(st2["cell_launches"], 1)),
+            "cell_share_of_step": cell_ms / t_ms, "peak_source": peak_src,
+            "alg_bytes_def": "per processing (2 r^3 + 6 r^2) s read + changed points * s written",
+            "kernel_timer": ("CUDA events around the persistent k_async launch on its stream, every timed solve"
+                             if async_mode and ev_ms > 0 else "%globaltimer span of the cell-kernel launches")}
+    work = {"rounds": st["rounds"], "grid_sweeps": st["grid_sweeps"], "cell_processings": st["cell_processings"],
+            "processings_per_cell": st["cell_processings"] / st["J"],
+            "sweeps_per_cell": st["cell_sweeps"] / st["J"],
+            "updates_per_point": st["point_updates"] / st["M"],
+            "writes_per_point": st["point_writes"] / st["M"],
+            "max_worklist": st["max_worklist"], "J": st["J"],
+            "grid_pass_equivalents": st["real_points_processed"] / st["M"],
+            "bytes_min_GBps": st["bytes_min"] / (t_ms * 1e-3) / 1e9,
+            "ms_ingest": st["ms_ingest"], "ms_loop": st["ms_loop"], "ms_egress": st["ms_egress"],
+            "ms_total_lib": st["ms_total"]}
+    rounds = float(np.mean([s["rounds"] for s in stats]))
+    launches_per_step = (5 if async_mode else
+                         4 + (launches + rounds if sweep else rounds * (1 if args.bin_width is None else 3)))
+    return dict(n=n, M=M, F=F, m=m, q=q, t_ms=t_ms, roof=roof, work=work, clk=clk.summary(),
+                launches_per_step=launches_per_step)
+
+
+def plumbing_test(args):
+    """CPU-only check of the multi-rank plumbing (tests/test_dist_cpu.py): gloo, a fixed fake
+    step time per rank, the max over ranks and the whole-job value; never a bench number."""
+    import torch.distributed as dist
+    rank, _, ws = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    t = 0.010 * (rank + 1)
+    tj = job_time(t, dist if ws > 1 else None, "cpu")
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": job_value(1000, ws, tj), "unit": UNIT,
+                          "n_gpus": ws, "ms_per_step": tj * 1e3, "data": "plumbing-test"}), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -236,9 +396,10 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=None, help="override n (reduced size; not a bench line)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-n", type=int, default=128, help="oracle sample size for --impl reference")
-    ap.add_argument("--cpu-n", type=int, default=256, help="oracle sample size for cpu_baseline")
+    ap.add_argument("--ref-n", type=int, default=128,
+                    help="--impl reference: side (intervals) of the sub-box of the input timed per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the fp64 sub-line of the C3 bench")
     ap.add_argument("--bin-width", type=float, default=None,
                     help="priority bin width (round modes; implies --loop-mode 2)")
     ap.add_argument("--loop-mode", type=int, default=None,
@@ -247,7 +408,12 @@ def main():
     ap.add_argument("--method", default="hcm", choices=["hcm", "dfsm", "dlsm"],
                     help="hcm: the product path (eik_solve); dfsm / dlsm: the paper's comparison "
                          "sweeping methods on the GPU (eik_solve_sweep, SURVEY 8(f) F2)")
+    ap.add_argument("--plumbing-test", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus, sys.argv[1:])
+    if args.plumbing_test:
+        return plumbing_test(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -255,6 +421,10 @@ def main():
     import paper_1306_4743_b200 as eik
 
     rank, local, ws = dist_env()
+    if ws > 1 and args.gpus not in (1, ws):
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {ws}")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"rank {rank}: local rank {local} but {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
@@ -269,80 +439,18 @@ def main():
         torch.cuda.synchronize()
 
     cfg, prec, r = WORKLOADS[args.config]
-    n, F, m, q = make_inputs(cfg, prec, dev, args.n)
-    M = (n + 1) ** 3
-    s_bytes = 4 if prec == "f32" else 8
     loop_mode = args.loop_mode if args.loop_mode is not None else (2 if args.bin_width is not None else None)
     solver = eik.Solver(device=local, bin_width=args.bin_width, loop_mode=loop_mode)
-    async_mode = loop_mode in (None, 0) and not sweep_method(args)
+    sweep = args.method != "hcm"
+    async_mode = loop_mode in (None, 0) and not sweep
     if async_mode:
         # CUDA events around the persistent cell-kernel launch, recorded by the library on the
         # launching stream inside every timed solve (the roofline's denominator)
         solver.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
-    U = torch.empty_like(F)
-    stream = torch.cuda.current_stream(dev)
-
-    sweep = args.method != "hcm"
-
-    def run_once():
-        if sweep:
-            solver.solve_sweep(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U, method=args.method)
-        else:
-            solver.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=U)
-
-    for _ in range(args.warmup):
-        run_once()
-
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stats = []
-    barrier()
-    with Clocks(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            run_once()
-            stats.append(solver.stats())
-        ev1.record(stream)
-        barrier()
-    t_ms = job_time(ev0.elapsed_time(ev1) / args.steps, pg, dev)
+    res = measure(eik, solver, cfg, prec, r, dev, args, sweep=sweep, async_mode=async_mode,
+                  barrier=barrier, pg=pg)
+    n, M, F, m, q, t_ms = res["n"], res["M"], res["F"], res["m"], res["q"], res["t_ms"]
     value = job_value(M, ws, t_ms * 1e-3)
-
-    # roofline of the dominant kernel (cell sweep): algorithmic bytes / its device time
-    cell_ms = float(np.mean([s["ms_cell_device"] for s in stats]))            # %globaltimer span
-    ev_ms = float(np.mean([s["ms_cell_events"] for s in stats]))              # CUDA events (async)
-    if async_mode and ev_ms > 0:
-        cell_ms = ev_ms
-    alg_bytes = float(np.mean([s["bytes_cell_alg"] for s in stats]))
-    launches = float(np.mean([s["cell_launches"] for s in stats]))
-    rounds = float(np.mean([s["rounds"] for s in stats]))
-    peak, peak_src = peaks()
-    achieved = alg_bytes / (cell_ms * 1e-3) / 1e9 if cell_ms > 0 else None
-    # event-timed cross-check of the same kernel (host-loop mode, CUDA events around launches)
-    st2 = {"ms_cell_events": 0.0, "cell_launches": 1}
-    if async_mode:
-        st2 = {"ms_cell_events": ev_ms, "cell_launches": 1}
-    elif not sweep:
-        # CUDA events around every round's cell-kernel launch in the host-driven loop
-        s2 = eik.Solver(device=local, loop_mode=1, bin_width=args.bin_width)
-        s2.set_option(eik.EIK_OPT_TIME_CELL_EVENTS, 1)
-        s2.solve(F, m, q, h=grid_h(cfg, n), cell_size=r, n=n, out=torch.empty_like(F))
-        st2 = s2.stats()
-        s2.close()
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"r01_ncu_{args.config}.json")
-    if os.path.exists(tp) and not sweep:   # ncu DRAM bytes of the cell kernel per processing x processings/launch
-        d = json.load(open(tp))["kcell_traffic"]
-        traffic = d["dram_bytes_per_processing"] * (stats[-1]["cell_processings"] / max(launches, 1))
-    st = stats[-1]
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": f"{'k_dsweep' if sweep else 'k_async' if async_mode else 'k_cell'}<{'float' if prec == 'f32' else 'double'},{r}>",
-            "alg_bytes_per_launch": alg_bytes / max(launches, 1),
-            "ms_per_launch_device": float(np.mean([s["ms_cell_device"] for s in stats])) / max(launches, 1),
-            "ms_per_launch_events": (st2["ms_cell_events"] / max(st2["cell_launches"], 1)),
-            "cell_share_of_step": cell_ms / t_ms, "peak_source": peak_src,
-            "alg_bytes_def": "per processing (2 r^3 + 6 r^2) s read + changed points * s written",
-            "kernel_timer": ("CUDA events around the persistent k_async launch on its stream, every timed solve"
-                             if async_mode and ev_ms > 0 else "%globaltimer span of the cell-kernel launches")}
 
     # e2e: the same solve through the C ABI with pinned HOST buffers, copies inside the timing
     e2e = None
@@ -365,13 +473,23 @@ def main():
                "timer": "host wall clock around the blocking C-ABI call (pinned buffers)",
                "transfers": "F and exit_mask copied H2D; exit_vals read in place at the exit points "
                             "(mapped pinned memory); U copied D2H"}
+        del Fh, mh, qh, Uh
+    del F, m, q
+    res.pop("F"), res.pop("m"), res.pop("q")
+
+    # the paper's default precision on the headline config, device-timed the same way
+    fp64 = None
+    if args.config == "C3" and not args.no_fp64 and not sweep and args.n is None:
+        r64 = measure(eik, solver, "C3", "f64", 16, dev, args, sweep=False, async_mode=async_mode,
+                      barrier=barrier, pg=pg)
+        fp64 = {"workload": "C3d: " + DESC["C3"] + ", fp64, cell size 16", "dtype": "f64",
+                "ms_per_step": r64["t_ms"], "value": job_value(r64["M"], ws, r64["t_ms"] * 1e-3),
+                "unit": UNIT, "roofline": r64["roof"], "work": r64["work"], "clocks": r64["clk"],
+                "gpu_launches": int(args.steps * r64["launches_per_step"])}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        Ms, secs = cpu_oracle_sample(cfg, args.cpu_n)
-        cpu = {"value": Ms / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"serial fp64 FMM oracle on the {cfg} formulas at n={args.cpu_n} "
-                         f"({Ms} points, {secs:.1f} s) on 1 of {os.cpu_count()} host cores"}
+    if rank == 0 and ws == 1 and not args.no_cpu and args.n is None:
+        cpu = cpu_baseline(cfg)
 
     if rank == 0:
         line = {
@@ -381,26 +499,18 @@ def main():
             "config": dict(config_block(cfg, prec, r, n), **({"solve": f"eik_solve_sweep ({args.method}): "
                            "ingest + whole-grid sweep loop (CUDA graph) + egress"} if sweep else {}),
                            **({"bin_width": args.bin_width} if args.bin_width is not None else {})),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": res["roof"], "cpu_baseline": cpu, "e2e": e2e,
             # per solve: init, ingest, (worklist build), egress + the loop's launches: fused
             # rounds = one k_cell each (k_select + k_cell + k_round_end otherwise); sweeping =
             # one k_dsweep per cell diagonal + k_sweep_end per sweep
             # async: init, ingest, seed, the persistent k_async, egress
-            "gpu_launches": int(args.steps * (5 if async_mode else
-                                              4 + (launches + rounds if sweep else
-                                                   rounds * (1 if args.bin_width is None else 3)))),
-            "clocks": clk.summary(),
+            "gpu_launches": int(args.steps * res["launches_per_step"]),
+            "clocks": res["clk"],
             "method": args.method,
-            "work": {"rounds": st["rounds"], "grid_sweeps": st["grid_sweeps"], "cell_processings": st["cell_processings"],
-                     "processings_per_cell": st["cell_processings"] / st["J"],
-                     "sweeps_per_cell": st["cell_sweeps"] / st["J"],
-                     "updates_per_point": st["point_updates"] / st["M"],
-                     "writes_per_point": st["point_writes"] / st["M"],
-                     "max_worklist": st["max_worklist"], "J": st["J"],
-                     "grid_pass_equivalents": st["real_points_processed"] / st["M"],
-                     "bytes_min_GBps": st["bytes_min"] / (t_ms * 1e-3) / 1e9,
-                     "ms_ingest": st["ms_ingest"], "ms_loop": st["ms_loop"], "ms_egress": st["ms_egress"]},
+            "work": res["work"],
         }
+        if fp64 is not None:
+            line["c3_fp64"] = fp64
         print(json.dumps(line), flush=True)
     solver.close()
     if pg is not None:

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EIK_ABI_VERSION 3   /* 3: eik_stats gained h2d_bytes, d2h_bytes */
+#define EIK_ABI_VERSION 4   /* 3: eik_stats gained h2d_bytes, d2h_bytes; 4: eik_get_trace, EIK_OPT_TRACE */
 
 typedef struct eik_ctx eik_ctx;
 
@@ -83,11 +83,14 @@ typedef enum {
                                 largest change is <= kappa.  kappa > 0 returns an
                                 approximation of the discrete solution (values >= it; P:1187
                                 gives no error bound)                                            */
-    EIK_OPT_CELL_KEY = 9     /* cell value of a tag (Alg. 1 line 9): 0 = Eq. (3), the smallest
+    EIK_OPT_CELL_KEY = 9,    /* cell value of a tag (Alg. 1 line 9): 0 = Eq. (3), the smallest
                                 newly updated inflow value, reset to +inf on removal [0];
                                 1 = the legacy Eq. (4): V_max + D / F(y), never
                                 reset.  Orders work only (bin width < inf, async readiness);
                                 the fixed point is the same                          */
+    EIK_OPT_TRACE = 10       /* diagnostics, async mode: record up to this many cell processings
+                                (cell, tagger, pop / swept / end times, sweeps, flags, generation)
+                                for eik_get_trace; 0 = off [0]                                  */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */
@@ -184,6 +187,15 @@ int eik_get_stats(const eik_ctx* ctx, eik_stats* out);
  * round r (round modes, r < 1024), out[2090], out[2091] cycles in tile loads / halo loads.
  * Copies min(n, 2092) values.  EIK_EINVAL if ctx/out is NULL or n < 0. */
 int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n);
+
+/* Processing trace of the last solve (EIK_OPT_TRACE > 0, async mode): copies up to
+ * max_entries entries of 8 uint32 each into out (host memory, 32 bytes per entry):
+ *   {cell, id of the processing that last tagged it (0xFFFFFFFF: seeded), t_pop, t_swept,
+ *    t_end, sweeps, state flags taken at the pop, activation generation}
+ * with times in ns since the solve's start (t_swept: sweeps and write-back done, before the
+ * neighbour tags; t_end: tags and release done).  The entry index is the processing id.
+ * Returns the number of entries copied (0 if tracing is off), or -EIK_EINVAL / -EIK_ECUDA. */
+int64_t eik_get_trace(const eik_ctx* ctx, uint32_t* out, int64_t max_entries);
 
 /* Message of the last failing call on ctx (owned by ctx; valid until its next call).
  * eik_last_error(NULL) returns the message of the last failed eik_create. */

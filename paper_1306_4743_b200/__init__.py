@@ -21,17 +21,18 @@ EIK_OK, EIK_EINVAL, EIK_ENOMEM, EIK_ECUDA, EIK_ENOTSUP, EIK_EINTERNAL = range(6)
 EIK_F32, EIK_F64 = 0, 1
 EIK_DFSM, EIK_DLSM = 0, 1          # eik_solve_sweep methods
 (EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS,
- EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS, EIK_OPT_TIMEOUT_S, EIK_OPT_KAPPA, EIK_OPT_CELL_KEY) = range(10)
+ EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS, EIK_OPT_TIMEOUT_S, EIK_OPT_KAPPA, EIK_OPT_CELL_KEY,
+ EIK_OPT_TRACE) = range(11)
 STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
                 4: "EIK_ENOTSUP", 5: "EIK_EINTERNAL"}
 
 # every symbol include/eik.h declares (checked by tests/test_abi.py)
 EXPORTS = ("eik_create", "eik_set_stream", "eik_set_option", "eik_solve", "eik_solve_host",
-           "eik_solve_sweep", "eik_get_stats", "eik_get_debug", "eik_last_error", "eik_destroy",
-           "eik_abi_version")
+           "eik_solve_sweep", "eik_get_stats", "eik_get_debug", "eik_get_trace", "eik_last_error",
+           "eik_destroy", "eik_abi_version")
 
 
-ABI_VERSION = 3   # include/eik.h EIK_ABI_VERSION (the EikStats layout below)
+ABI_VERSION = 4   # include/eik.h EIK_ABI_VERSION (the EikStats layout below)
 
 
 class EikStats(ctypes.Structure):
@@ -81,6 +82,8 @@ def _load():
     lib.eik_get_stats.restype = I
     lib.eik_get_debug.argtypes = [P, P, I]
     lib.eik_get_debug.restype = I
+    lib.eik_get_trace.argtypes = [P, P, I64]
+    lib.eik_get_trace.restype = I64
     lib.eik_last_error.argtypes = [P]
     lib.eik_last_error.restype = ctypes.c_char_p
     lib.eik_destroy.argtypes = [P]
@@ -255,6 +258,16 @@ class Solver:
                 "cyc_stage": int(a[36]), "cyc_mask": int(a[37]), "cyc_steps": int(a[38]),
                 "cyc_writeback": int(a[39]), "list_iters": int(a[40]), "defers": int(a[41]),
                 "cyc_tile": int(a[2090]), "cyc_halo": int(a[2091])}
+
+    def trace(self, max_entries: int = 1 << 26):
+        """Processing trace of the last async solve (EIK_OPT_TRACE): numpy uint32 [n, 8] rows
+        {cell, tagger id, t_pop, t_swept, t_end, sweeps, flags, generation} (ns)."""
+        import numpy as np
+        a = np.zeros((max_entries, 8), dtype=np.uint32)
+        n = lib.eik_get_trace(self._ctx, a.ctypes.data, max_entries)
+        if n < 0:
+            raise self._err(-n)
+        return a[:n].copy()
 
     def stats(self) -> dict:
         s = EikStats()

@@ -41,6 +41,10 @@ struct eik_ctx {
     double kappa = 0.0;
     int legacy_key = 0;
     double timeout_s = 120.0;
+    uint32_t trace_cap = 0;       // EIK_OPT_TRACE: processings traced (0 = off)
+    uint4* trace = nullptr;
+    uint32_t* tagger = nullptr;
+    size_t tagger_cap = 0;
     cudaEvent_t cev[2] = {nullptr, nullptr};
     double ms_cell_events = 0;
     // scratch
@@ -62,6 +66,7 @@ struct eik_ctx {
     Ctl* ctl_host = nullptr;      // pinned
     // plane tables per r (index 0: r=4, 1: r=8, 2: r=16)
     uint16_t* plane_tab[3] = {nullptr, nullptr, nullptr};
+    uint32_t* tab16 = nullptr;    // r = 16 packed per-direction plane table (sweep16)
     // host-pointer staging (eik_solve_host)
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -129,6 +134,33 @@ static void make_plane_table(int r, int nt, std::vector<uint16_t>& tab)
     }
 }
 
+// packed per-direction wavefront table of an r = 16 cell (sweep16, eik_kernels.cuh): for
+// direction d, plane s of the reflected coordinates (a', b', c'), thread t: the t-th point of
+// the canonical plane list above, reflected into physical coordinates (a, b, c) -- its box
+// index, the neighbours that exist in canonical orientation, its point index
+static void make_tab16(int nt, std::vector<uint32_t>& tab)
+{
+    const int r = 16, npl = 3 * r - 2, rows = npl + 3;
+    tab.assign((size_t)8 * rows * nt, T16_DUMMY);
+    for (int d = 0; d < 8; ++d)
+        for (int s = 0; s < npl; ++s) {
+            int t = 0;
+            for (int c = 0; c < r; ++c)
+                for (int b = 0; b < r; ++b) {
+                    const int a = s - b - c;
+                    if (a < 0 || a >= r) continue;
+                    const int pa = (d & 1) ? r - 1 - a : a, pb = (d & 2) ? r - 1 - b : b,
+                              pc = (d & 4) ? r - 1 - c : c;
+                    const uint32_t q = (uint32_t)((pa + 1) + (r + 2) * (pb + 1) + (r + 2) * (r + 2) * (pc + 1));
+                    const uint32_t p = (uint32_t)(pa + r * pb + r * r * pc);
+                    const uint32_t bm = (a < r - 1 ? 1u : 0u) | (a > 0 ? 2u : 0u) | (b < r - 1 ? 4u : 0u) |
+                                        (b > 0 ? 8u : 0u) | (c < r - 1 ? 16u : 0u) | (c > 0 ? 32u : 0u);
+                    tab[((size_t)d * rows + s) * nt + t++] = q | (bm << 13) | (p << 19);
+                }
+            if (t > nt) std::abort();
+        }
+}
+
 extern "C" int eik_abi_version(void) { return EIK_ABI_VERSION; }
 
 extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
@@ -168,6 +200,12 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
         make_plane_table(rs[t], nts[t], tab);
         CK(cudaMalloc(&ctx->plane_tab[t], tab.size() * sizeof(uint16_t)));
         CK(cudaMemcpy(ctx->plane_tab[t], tab.data(), tab.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    }
+    {
+        std::vector<uint32_t> tab;
+        make_tab16(CellCfg<16>::NT, tab);
+        CK(cudaMalloc(&ctx->tab16, tab.size() * sizeof(uint32_t)));
+        CK(cudaMemcpy(ctx->tab16, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
     // opt in to > 48 KB dynamic shared memory for the cell kernels
     CK(cudaFuncSetAttribute(k_cell<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
@@ -225,9 +263,12 @@ extern "C" void eik_destroy(eik_ctx* ctx)
     if (ctx->gexec_sw) cudaGraphExecDestroy(ctx->gexec_sw);
     free_scratch(ctx);
     cudaFree(ctx->stage);
+    cudaFree(ctx->trace);
+    cudaFree(ctx->tagger);
     cudaFree(ctx->ctl);
     cudaFreeHost(ctx->ctl_host);
     for (int t = 0; t < 3; ++t) cudaFree(ctx->plane_tab[t]);
+    cudaFree(ctx->tab16);
     for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
     for (int i = 0; i < 2; ++i) if (ctx->cev[i]) cudaEventDestroy(ctx->cev[i]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -287,6 +328,20 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         if (!(value > 0)) return fail(ctx, EIK_EINVAL, "timeout must be > 0 s");
         ctx->timeout_s = value;
         return EIK_OK;
+    case EIK_OPT_TRACE:
+        if (!(value >= 0) || value > 1e8) return fail(ctx, EIK_EINVAL, "trace capacity must be in [0, 1e8]");
+        if ((uint32_t)value != ctx->trace_cap) {
+            CK(cudaSetDevice(ctx->device));
+            if (ctx->stream) CK(cudaStreamSynchronize(ctx->stream));
+            cudaFree(ctx->trace);
+            ctx->trace = nullptr;
+            ctx->trace_cap = 0;
+            if (value >= 1) {
+                CK(cudaMalloc(&ctx->trace, (size_t)value * 2 * sizeof(uint4)));
+                ctx->trace_cap = (uint32_t)value;
+            }
+        }
+        return EIK_OK;
     case EIK_OPT_MAX_SWEEPS:
         if (!(value >= -1) || value > 1e6) return fail(ctx, EIK_EINVAL, "max sweeps must be >= -1");
         ctx->max_sweeps = (int)value;
@@ -319,6 +374,18 @@ extern "C" int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n)
     for (int i = 44 + 2048; i < n && i < 44 + 4096; ++i) out[i] = ctx->ctl_host->rtrace2[i - 44 - 2048];
     for (int i = 44 + 4096; i < n && i < 44 + 4096 + 12; ++i) out[i] = (&ctx->ctl_host->lstat[0][0])[i - 44 - 4096];
     return EIK_OK;
+}
+
+extern "C" int64_t eik_get_trace(const eik_ctx* ctx, uint32_t* out, int64_t max_entries)
+{
+    if (!ctx || (!out && max_entries > 0) || max_entries < 0) return -EIK_EINVAL;
+    if (!ctx->trace || !ctx->have_stats) return 0;
+    int64_t n = ctx->ctl_host->trace_n;
+    if (n > (int64_t)ctx->trace_cap) n = ctx->trace_cap;
+    if (n > max_entries) n = max_entries;
+    if (n > 0 && cudaMemcpy(out, ctx->trace, (size_t)n * 2 * sizeof(uint4), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -EIK_ECUDA;
+    return n;
 }
 
 extern "C" const char* eik_last_error(const eik_ctx* ctx)
@@ -434,6 +501,19 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     ca.defer_delta = isinf(ctx->bin_width) ? 0.f : (float)ctx->bin_width;
     CK(cudaMemsetAsync(ctx->wl0, 0xff, ctx->ring_cap * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->gen, 0, (size_t)J * 4, ctx->stream));
+    if (ctx->trace) {
+        if ((size_t)J > ctx->tagger_cap) {
+            cudaFree(ctx->tagger);
+            ctx->tagger = nullptr;
+            ctx->tagger_cap = 0;
+            CK(cudaMalloc(&ctx->tagger, (size_t)J * 4));
+            ctx->tagger_cap = (size_t)J;
+        }
+        CK(cudaMemsetAsync(ctx->tagger, 0xff, (size_t)J * 4, ctx->stream));
+        ca.trace = ctx->trace;
+        ca.trace_cap = ctx->trace_cap;
+        ca.tagger = ctx->tagger;
+    }
     k_seed_queue<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
     const bool te = ctx->time_cell_events != 0;   // CUDA events around the persistent launch
@@ -715,6 +795,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.state = ctx->state;
     const int ri = rindex_of(r);
     ca.plane_tab = ctx->plane_tab[ri];
+    ca.tab16 = ctx->tab16;
     ca.Vt = ctx->Vt;
     ca.Ht = ctx->Ht;
     // automatic sweep cap: rounds last as long as their slowest processing, so the round modes

@@ -252,6 +252,7 @@ struct Ctl {
     unsigned long long sweep_writes;   // strict decreases in the current sweep
     uint32_t sweep_dmax;          // largest value change of the current sweep (float bits, up)
     float kappa_f;                // early termination threshold of the sweeps
+    uint32_t trace_n;             // async mode processing trace (EIK_OPT_TRACE): entries written
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -544,6 +545,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_PARITY
 #define EIK_PARITY 1
 #endif
+#ifndef EIK_SWEEP16
+#define EIK_SWEEP16 1   // r = 16, kappa = 0: the packed-table wavefront step (sweep16)
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -595,6 +599,7 @@ struct CellArgs {
     uint32_t* state;
     uint32_t* gen;               // async mode: BFS generation of each cell (readiness mode 5)
     const uint16_t* plane_tab;   // [NPL + 3][NT] canonical point of thread t in plane s (0xFFFF: none)
+    const uint32_t* tab16;       // r = 16: [8][NPL + 3][NT] packed per-direction plane table (sweep16)
     void* Vt;
     const void* Ht;
     int64_t n1;
@@ -620,6 +625,12 @@ struct CellArgs {
                                      // its last CTA ends the round (no k_select / k_round_end)
     int32_t graph;                   // fused + CUDA graph: the last CTA sets the WHILE condition
     unsigned long long cond;         // cudaGraphConditionalHandle of that WHILE node
+    // async-mode processing trace (diagnostics, EIK_OPT_TRACE; null = off): per processing two
+    // uint4 {cell, processing id of its last tagger, t_pop, t_swept} {t_end, sweeps, flags, gen}
+    // (ns since the solve's start), tagger[c] = id of the last processing that tagged c
+    uint4* trace;
+    uint32_t trace_cap;
+    uint32_t* tagger;
 };
 
 // preferred sweep directions from the inflow faces (reading R20): a direction
@@ -873,6 +884,161 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     return bwd;
 }
 
+// ---- r = 16 wavefront sweep with a packed per-direction plane table -------------------------
+// tab16[d][s][t] (built on the host, eik.cu make_tab16) describes the t-th point of plane s of
+// direction d: bits 0-12 its box index q = (a+1) + 18 (b+1) + 324 (c+1), bits 13-18 the
+// neighbours that exist in the canonical (reflected) orientation of d (bit 0 forward x, 1
+// backward x, 2/3 y, 4/5 z), bits 19-31 its point index p = a + 16 b + 256 c.  A thread with no
+// point on a plane gets T16_DUMMY: a halo box index (reads only), no neighbours, and the flag
+// byte act[T16_DUMMY_P], which is 0 for the whole processing -- so every lane runs the same
+// straight-line step (no divergence, one warp vote skips the local solve of an idle warp).
+// Against sweep_dir this removes the per-step coordinate arithmetic (box offset, reflection,
+// border tests) and the branches; the activations are predicated stores at compile-time
+// offsets.  kappa = 0 only (the exact path; kappa > 0 runs sweep_dir).
+static constexpr uint32_t T16_DUMMY_P = 16 * 16 * 16 + 1;                       // act[R3 + 1]
+static constexpr uint32_t T16_DUMMY = (1u + 18u + 324u) | (T16_DUMMY_P << 19);   // box (-1, 0, 0)
+static constexpr int T16_ROWS = 3 * 16 - 2 + 3;   // NPL + 3 trailing empty planes
+
+template <typename T, int DIR>
+__device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* __restrict__ tab,
+                                            unsigned long long pm, bool ungated, uint32_t& nupd,
+                                            uint32_t& nwr, uint32_t& nsteps)
+{
+    using C = CellCfg<16>;
+    constexpr int NPL = C::NPL, NT = C::NT, R3 = C::R3;
+    constexpr int TS = (int)sizeof(T);
+    constexpr bool HG = CellSmem<T, 16>::HG;
+    // forward neighbour offsets (canonical forward = physical +1 unless the axis is reflected)
+    constexpr int sx = (DIR & 1) ? -1 : 1, sy = (DIR & 2) ? -1 : 1, sz = (DIR & 4) ? -1 : 1;
+    // (unsigned: address arithmetic wraps modulo 2^32, a negative offset subtracts)
+    constexpr uint32_t oxq = (uint32_t)(sx * TS), oyq = (uint32_t)(sy * C::RP * TS),
+                       ozq = (uint32_t)(sz * C::RP2 * TS);                              // box bytes
+    constexpr uint32_t oxp = (uint32_t)sx, oyp = (uint32_t)(sy * 16), ozp = (uint32_t)(sz * 256);   // flag bytes
+    const T INF = dinf<T>();
+    const uint32_t vb = smem_u32(M.V);
+    const uint32_t hb = HG ? 0u : smem_u32(M.H);
+    const T* __restrict__ hg = M.Hg;
+    const uint32_t ab = smem_u32(M.act);
+    const uint32_t* __restrict__ tp = tab + DIR * T16_ROWS * NT + threadIdx.x;
+    uint32_t one;
+    asm("mov.u32 %0, 1;" : "=r"(one));
+    bool fwd = false;
+    uint32_t bwd = 0;
+    int s = __ffsll((long long)pm) - 1;
+    unsigned long long pmr = pm >> s;   // pm >> (current plane)
+    uint32_t en = __ldg(tp + s * NT);
+    uint32_t en1 = __ldg(tp + (s + 1) * NT);
+    tp += (s + 2) * NT;
+#define EIK16_HF(e_) (HG ? (((e_) >> 19) < (uint32_t)R3 ? __ldg(hg + ((e_) >> 19)) : INF)          \
+                         : lds<T>(hb + ((e_) >> 19) * TS))
+    T hn = EIK16_HF(en);
+#define EIK16_PREFETCH()                                                                   \
+    {                                                                                      \
+        en = en1;                                                                          \
+        hn = EIK16_HF(en);                                                                 \
+        en1 = __ldg(tp);                                                                   \
+        tp += NT;                                                                          \
+    }
+#define EIK16_MARK(ue_, hf_)                                                               \
+    {                                                                                      \
+        EIK_CHECK(((ue_) >> 19) < (uint32_t)R3, "sweep16 changed point");                  \
+        if constexpr (HG) atomicOr(&M.chg[(ue_) >> 24], 1u << (((ue_) >> 19) & 31));      \
+        else sts(hb + ((ue_) >> 19) * TS, -(hf_));   /* sign bit = changed */              \
+    }
+    if (ungated) {
+        // first sweep of a fresh cell: every point of every plane, only the activations behind
+        // the wavefront are recorded (forward neighbours are visited later in this sweep)
+        for (; s < NPL; ++s) {
+            const uint32_t ue = en;
+            const T hs = hn;
+            EIK16_PREFETCH()
+            const uint32_t qa = vb + (ue & 0x1fffu) * TS;
+            const uint32_t fa = ab + (ue >> 19);
+            const T v = lds<T>(qa);
+            const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
+            const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
+            const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
+            sts_u8(fa, 0u);                                                // Alg. 2 line 4
+            const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
+            const T hf = fabs(hs);
+            const bool gate = ue != T16_DUMMY && hf < INF && vmin(mx, vmin(my, mz)) < v;
+            if (__any_sync(0xffffffffu, gate)) {
+                const T u = local_solve_fast<T>(mx, my, mz, hf);
+                const bool chg = gate && u < v;
+                nupd += gate;
+                nwr += chg;
+                if (chg) {
+                    sts(qa, u);
+                    EIK16_MARK(ue, hf)
+                }
+                const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
+                const bool bxa = (bm & (2u << 13)) && xb > u, bya = (bm & (8u << 13)) && yb > u,
+                           bza = (bm & (32u << 13)) && zb > u;
+                if (bxa) sts_u8(fa - oxp, one);
+                if (bya) sts_u8(fa - oyp, one);
+                if (bza) sts_u8(fa - ozp, one);
+                bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
+            }
+            __syncthreads();
+            ++nsteps;
+        }
+        pmr = 0;
+    }
+    for (; s < NPL; ++s, pmr >>= 1) {
+        if (!(((uint32_t)pmr & 1u) | (uint32_t)fwd)) {
+            if (pmr == 0ull) break;
+            EIK16_PREFETCH()
+            continue;
+        }
+        const uint32_t ue = en;
+        const T hs = hn;
+        EIK16_PREFETCH()
+        const uint32_t qa = vb + (ue & 0x1fffu) * TS;
+        const uint32_t fa = ab + (ue >> 19);
+        // flag and the seven box values in one shared-memory round trip
+        const uint32_t fl = lds_u8(fa);
+        const T v = lds<T>(qa);
+        const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
+        const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
+        const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
+        const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
+        const T hf = fabs(hs);
+        sts_u8(fa, 0u);   // Alg. 2 line 4 (unconditional: nothing activates plane s during step s)
+        const bool gate = fl && hf < INF && vmin(mx, vmin(my, mz)) < v;   // active, not fixed, can gain
+        bool myfwd = false;
+        if (__any_sync(0xffffffffu, gate)) {
+            const T u = local_solve_fast<T>(mx, my, mz, hf);                // line 5
+            const bool chg = gate && u < v;                                 // line 6
+            nupd += gate;
+            nwr += chg;
+            if (chg) {
+                sts(qa, u);                                                 // line 7
+                EIK16_MARK(ue, hf)
+            }
+            // lines 8-13: activate larger in-cell neighbours (the cross-border "currently
+            // downwind" test is done once per processing)
+            const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
+            const bool fxa = (bm & (1u << 13)) && xf > u, bxa = (bm & (2u << 13)) && xb > u;
+            const bool fya = (bm & (4u << 13)) && yf > u, bya = (bm & (8u << 13)) && yb > u;
+            const bool fza = (bm & (16u << 13)) && zf > u, bza = (bm & (32u << 13)) && zb > u;
+            if (fxa) sts_u8(fa + oxp, one);
+            if (bxa) sts_u8(fa - oxp, one);
+            if (fya) sts_u8(fa + oyp, one);
+            if (bya) sts_u8(fa - oyp, one);
+            if (fza) sts_u8(fa + ozp, one);
+            if (bza) sts_u8(fa - ozp, one);
+            myfwd = fxa | fya | fza;
+            bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
+        }
+        fwd = __syncthreads_or(myfwd);
+        ++nsteps;
+    }
+#undef EIK16_HF
+#undef EIK16_PREFETCH
+#undef EIK16_MARK
+    return bwd;
+}
+
 // Stage cell c (tile coordinates cx, cy, cz) into shared memory: the tile and its hf go out
 // as cp.async (no registers), the halo N(c) as L2 loads issued right behind them -- one
 // memory round trip for all of it; returns when this thread's copies have landed (the caller
@@ -1026,6 +1192,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
         S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
+        sA[R3 + 1] = 0;   // sweep16's dummy flag byte (T16_DUMMY_P): never set
     }
     // phase timers live in shared memory, written by thread 0 only (no registers held
     // across the sweeps): tm = {start, tile staged, halo staged, init done, mask, steps, list
@@ -1385,6 +1552,17 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             const bool ungated = first && nact >= R3 / 8;
             if constexpr (R < EIK_DIR_TEMPLATE_MIN_R) {
                 bwd = sweep_dir<T, R, -1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_, dir);
+            } else if (R == 16 && EIK_SWEEP16 && kap == T(0)) {
+                if constexpr (R == 16) switch (dir) {
+                case 0: bwd = sweep16<T, 0>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                case 1: bwd = sweep16<T, 1>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                case 2: bwd = sweep16<T, 2>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                case 3: bwd = sweep16<T, 3>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                case 4: bwd = sweep16<T, 4>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                case 5: bwd = sweep16<T, 5>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                case 6: bwd = sweep16<T, 6>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                default: bwd = sweep16<T, 7>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
+                }
             } else switch (dir) {
             case 0: bwd = sweep_dir<T, R, 0>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
             case 1: bwd = sweep_dir<T, R, 1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
@@ -1683,6 +1861,7 @@ k_async(CellArgs A)
     Ctl* ctl = A.ctl;
     uint32_t* ring = A.wl0;
     if (tid == 0) atomicMin(&ctl->t_start, gtimer());
+    uint32_t tr_pid = 0, tr_tag = 0, tr_pop = 0, tr_swept = 0;   // processing trace (thread 0)
     for (;;) {
         if (tid < 32) {   // warp 0 pops the next cell; the other warps wait at the barrier
             const int lane = tid;
@@ -1762,6 +1941,11 @@ k_async(CellArgs A)
                 S.cell = got;
                 S.flags = fl;
                 S.stat[0] = S.stat[1] = S.stat[2] = 0;
+                if (A.trace && got != Q_EMPTY) {   // (thread 0's registers)
+                    tr_pid = atomicAdd(&ctl->trace_n, 1u);
+                    tr_tag = __ldcg(&A.tagger[got]);
+                    tr_pop = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
+                }
             }
         }
         __syncthreads();
@@ -1770,6 +1954,8 @@ k_async(CellArgs A)
         const long long t0 = clock64();
         unsigned long long nsw = 0;
         cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
+        if (A.trace && tid == 0) tr_swept = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
+        if (tid < 32) tr_pid = __shfl_sync(0xffffffffu, tr_pid, 0);
         __threadfence();   // value stores before the re-activations
         __syncthreads();
         // re-activations first, then the cell's own release: a neighbour waiting for this
@@ -1780,6 +1966,7 @@ k_async(CellArgs A)
             if (nc >= 0) {
                 atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
                 if (A.defer >= 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
+                if (A.trace) A.tagger[nc] = tr_pid;
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
                 if (!(old & (ST_QUEUED | ST_RUNNING))) {
                     q_push(ctl, ring, A.qmask, (uint32_t)nc);
@@ -1805,6 +1992,11 @@ k_async(CellArgs A)
                 atomicAdd(&ctl->dbg[0], cyc);
                 atomicMax(&ctl->dbg[1], cyc);
                 atomicAdd(&ctl->dbg[3], 1ull);
+            }
+            if (A.trace && tr_pid < A.trace_cap) {
+                const uint32_t te = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
+                A.trace[2 * tr_pid] = make_uint4(c, tr_tag, tr_pop, tr_swept);
+                A.trace[2 * tr_pid + 1] = make_uint4(te, (uint32_t)nsw, S.flags, __ldcg(&A.gen[c]));
             }
             __threadfence();
             atomicSub(&ctl->pending, 1u);

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(eik.lib, name), name
     assert set(_declared()) == set(eik.EXPORTS)
-    assert eik.lib.eik_abi_version() == 3
+    assert eik.lib.eik_abi_version() == eik.ABI_VERSION
 
 
 def test_lib_is_sm100a_cubin():

@@ -60,6 +60,7 @@ struct eik_ctx {
     uint32_t* pend = nullptr;
     uint32_t* pdir = nullptr;
     uint32_t* gen = nullptr;
+    uint32_t* wait = nullptr;
     size_t cell_cap = 0;
     size_t ring_cap = 0;
     Ctl* ctl = nullptr;
@@ -83,7 +84,7 @@ struct eik_ctx {
     std::vector<uint32_t> diag_off_h;
     uint8_t* cact = nullptr;
     // events
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     eik_stats stats{};
     bool have_stats = false;
 };
@@ -191,7 +192,7 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     }
     CK(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&ctx->ctl_host, sizeof(Ctl)));
-    for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&ctx->ev[i]));
+    for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ctx->ev[i]));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreate(&ctx->cev[i]));
     const int rs[3] = {4, 8, 16};
     const int nts[3] = {CellCfg<4>::NT, CellCfg<8>::NT, CellCfg<16>::NT};
@@ -241,7 +242,7 @@ static void free_scratch(eik_ctx* ctx)
 {
     cudaFree(ctx->Vt); cudaFree(ctx->Ht);
     cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
-    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen); cudaFree(ctx->pdir);
+    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen); cudaFree(ctx->wait); cudaFree(ctx->pdir);
     cudaFree(ctx->diag_cells); cudaFree(ctx->diag_off); cudaFree(ctx->cact);
     ctx->diag_cells = ctx->diag_off = nullptr;
     ctx->cact = nullptr;
@@ -249,6 +250,7 @@ static void free_scratch(eik_ctx* ctx)
     ctx->pend = nullptr;
     ctx->pdir = nullptr;
     ctx->gen = nullptr;
+    ctx->wait = nullptr;
     ctx->Vt = ctx->Ht = nullptr;
     ctx->key = ctx->state = ctx->wl0 = ctx->wl1 = ctx->proc_cell = ctx->proc_flags = nullptr;
     ctx->tile_bytes = ctx->cell_cap = 0;
@@ -269,7 +271,7 @@ extern "C" void eik_destroy(eik_ctx* ctx)
     cudaFreeHost(ctx->ctl_host);
     for (int t = 0; t < 3; ++t) cudaFree(ctx->plane_tab[t]);
     cudaFree(ctx->tab16);
-    for (int i = 0; i < 4; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
+    for (int i = 0; i < 5; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
     for (int i = 0; i < 2; ++i) if (ctx->cev[i]) cudaEventDestroy(ctx->cev[i]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     (void)cudaGetLastError();
@@ -416,6 +418,7 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
         CK(cudaMalloc(&ctx->pend, J * 512));   // R^3 / 8 bytes per cell at r = 16
         CK(cudaMalloc(&ctx->pdir, J * 4));     // sweep-direction state at a cap
         CK(cudaMalloc(&ctx->gen, J * 4));
+        CK(cudaMalloc(&ctx->wait, J * 4));
         CK(cudaMalloc(&ctx->diag_cells, J * 4));
         CK(cudaMalloc(&ctx->cact, J));
         ctx->cell_cap = J;
@@ -501,6 +504,8 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     ca.defer_delta = isinf(ctx->bin_width) ? 0.f : (float)ctx->bin_width;
     CK(cudaMemsetAsync(ctx->wl0, 0xff, ctx->ring_cap * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->gen, 0, (size_t)J * 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->wait, 0, (size_t)J * 4, ctx->stream));
+    ca.wait = ctx->wait;
     if (ctx->trace) {
         if ((size_t)J > ctx->tagger_cap) {
             cudaFree(ctx->tagger);
@@ -776,12 +781,9 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     }
     if (method < 0 && ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());
-    // input validation result (device-detected errors return before touching U_out)
-    CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (ctx->ctl_host->err & 1u) return fail(ctx, EIK_EINVAL, "F has a negative, NaN or infinite value");
-    if (ctx->ctl_host->err & 2u) return fail(ctx, EIK_EINVAL, "an exit value q is negative, NaN or infinite");
-    if (ctx->ctl_host->n_exits == 0) return fail(ctx, EIK_EINVAL, "no exit point (exit_mask is all zero)");
+    // No host round-trip here: a device-detected input error (ctl->err, no exit) makes the
+    // seeding kernels enqueue nothing, the loop does no work and k_egress returns without
+    // touching U_out; the status is read once, after egress.
     CK(cudaEventRecord(ctx->ev[1], s));
 
     CellArgs ca;
@@ -814,21 +816,33 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     st = method < 0 ? run_loop<T>(ctx, r, J, ca) : run_sweeps<T>(ctx, r, J, ca, method);
     if (st) return st;
     CK(cudaEventRecord(ctx->ev[2], s));
-    // host-side guard against a device loop that never returns (the device watchdog covers
-    // the scheduler; this covers everything else): poll the loop-end event with a deadline
+    {
+        const int64_t nv = ((n1 + 3) / 4) * n1;   // vectors per z-plane
+        const int bx = (int)((nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64);
+        const int by = (int)(n1 < 65535 ? n1 : 65535);
+        k_egress<T><<<dim3(bx, by), 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M, ctx->ctl);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[3], s));
+    CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ctx->ev[4], s));
+    // the one wait of the solve, with a host-side guard against a device loop that never
+    // returns (the device watchdog covers the scheduler; this covers everything else): spin on
+    // the event for the first 20 ms, then poll every 100 us until the deadline
     {
         const double limit_s = ctx->timeout_s + 30.0;
         struct timespec t0, t1;
         clock_gettime(CLOCK_MONOTONIC, &t0);
         for (;;) {
-            const cudaError_t q = cudaEventQuery(ctx->ev[2]);
-            if (q == cudaSuccess) break;
-            if (q != cudaErrorNotReady) CK(q);
+            const cudaError_t qe = cudaEventQuery(ctx->ev[4]);
+            if (qe == cudaSuccess) break;
+            if (qe != cudaErrorNotReady) CK(qe);
             clock_gettime(CLOCK_MONOTONIC, &t1);
-            if ((t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec) > limit_s) {
+            const double el = (t1.tv_sec - t0.tv_sec) + 1e-9 * (t1.tv_nsec - t0.tv_nsec);
+            if (el > limit_s) {
                 // read the control block through a side stream while the loop still runs
                 cudaStream_t side;
-                Ctl snap;
+                Ctl snap{};
                 if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess) {
                     cudaMemcpyAsync(&snap, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, side);
                     cudaStreamSynchronize(side);
@@ -839,11 +853,15 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
                             limit_s, snap.pending, snap.q_head, snap.q_tail, snap.rounds,
                             (unsigned long long)snap.processings);
             }
-            usleep(200);
+            if (el > 0.02) usleep(100);
         }
     }
-    CK(cudaMemcpyAsync(ctx->ctl_host, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (ctx->ctl_host->err & 1u) return fail(ctx, EIK_EINVAL, "F has a negative, NaN or infinite value");
+    if (ctx->ctl_host->err & 2u) return fail(ctx, EIK_EINVAL, "an exit value q is negative, NaN or infinite");
+    if (ctx->ctl_host->err & 16u)
+        return fail(ctx, EIK_EINVAL, "h/F out of the supported range of %s (%s) at some F > 0 point",
+                    sizeof(T) == 4 ? "fp32" : "fp64", sizeof(T) == 4 ? "2^-60 .. 2^60" : "2^-500 .. 2^500");
+    if (ctx->ctl_host->n_exits == 0) return fail(ctx, EIK_EINVAL, "no exit point (exit_mask is all zero)");
     if (ctx->ctl_host->err & 4u)
         return fail(ctx, EIK_EINTERNAL, "max %s (%u) exceeded", method < 0 ? "rounds" : "sweeps", ctx->max_rounds);
     if (ctx->ctl_host->err & 8u)
@@ -853,15 +871,6 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
                     (unsigned long long)ctx->ctl_host->processings);
     if (ctx->ctl_host->abort)
         return fail(ctx, EIK_EINTERNAL, "processing limit exceeded (async scheduler)");
-    {
-        const int64_t nv = ((n1 + 3) / 4) * n1;   // vectors per z-plane
-        const int bx = (int)((nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64);
-        const int by = (int)(n1 < 65535 ? n1 : 65535);
-        k_egress<T><<<dim3(bx, by), 256, 0, s>>>(g, (const T*)ctx->Vt, (T*)U, M);
-    }
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ctx->ev[3], s));
-    CK(cudaEventSynchronize(ctx->ev[3]));
 
     const Ctl& hc = *ctx->ctl_host;
     eik_stats& S = ctx->stats;

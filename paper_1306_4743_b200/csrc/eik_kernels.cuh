@@ -391,7 +391,12 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
                             atomicOr(&state[cc[f2]], FLAG_INIT);
                         }
                 } else if (fl > T(0)) {
-                    hh[l] = h / fl;   // +inf for subnormal-overflow: treated as impassable
+                    hh[l] = h / fl;
+                    // h/F must keep hf^2 normal and 3 hf^2 finite in T (the local solve squares
+                    // it): fp32 [2^-60, 2^60], fp64 [2^-500, 2^500]; outside -> EIK_EINVAL
+                    const T lo = sizeof(T) == 4 ? T(8.673617379884035e-19) : T(3.054936363499605e-151);
+                    const T hi = sizeof(T) == 4 ? T(1.152921504606847e18) : T(3.273390607896142e150);
+                    if (!(hh[l] >= lo && hh[l] <= hi)) atomicOr(&ctl->err, 16u);
                 }
             }
             Vec4T<T>::st(&Vt[p0[u]], vv);
@@ -417,6 +422,7 @@ __global__ void k_init_cells(uint32_t* key, uint32_t* state, int64_t J, Ctl* ctl
 __global__ void k_build_wl(const uint32_t* __restrict__ key, const uint32_t* __restrict__ state,
                            uint32_t* wl0, Ctl* ctl, int64_t J)
 {
+    if (__ldcg(&ctl->err) != 0u || __ldcg(&ctl->n_exits) == 0u) return;   // invalid input: no work
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < J;
          base += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = base + threadIdx.x;
@@ -598,6 +604,7 @@ struct CellArgs {
     uint32_t* key;
     uint32_t* state;
     uint32_t* gen;               // async mode: BFS generation of each cell (readiness mode 5)
+    uint32_t* wait;              // async mode: bit f = the neighbour across face f is parked on this cell
     const uint16_t* plane_tab;   // [NPL + 3][NT] canonical point of thread t in plane s (0xFFFF: none)
     const uint32_t* tab16;       // r = 16: [8][NPL + 3][NT] packed per-direction plane table (sweep16)
     void* Vt;
@@ -1849,6 +1856,17 @@ __device__ __forceinline__ void q_push(Ctl* ctl, uint32_t* ring, uint32_t qmask,
     while (atomicCAS(&ring[slot], Q_EMPTY, c) != Q_EMPTY) __nanosleep(32);
 }
 
+// re-queue a cell that is already counted in pending (a deferral, or a parked cell)
+__device__ __forceinline__ void q_repush(Ctl* ctl, uint32_t* ring, uint32_t qmask, uint32_t c)
+{
+    const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & qmask;
+    while (atomicCAS(&ring[slot], Q_EMPTY, c) != Q_EMPTY) __nanosleep(32);
+}
+
+#ifndef EIK_PARK
+#define EIK_PARK 0   // 1: a cell deferred by a running neighbour waits on it instead of cycling the ring (measured: C3 7.17 -> 7.57 ms, C5 35.7 -> 36.4; off)
+#endif
+
 template <typename T, int R>
 __global__ void __launch_bounds__(CellCfg<R>::NT, MinBlocks<T, R>::value)
 k_async(CellArgs A)
@@ -1898,15 +1916,16 @@ k_async(CellArgs A)
                 // readiness (the heap order of Alg. 3 approximated locally): lane f checks the
                 // neighbour across face f -- all loads of the six checks in one round trip --
                 // and v is re-queued while a neighbour runs or is queued ahead of it
-                bool d = false;
+                bool d = false, drun = false;
+                int64_t nb = -1;
                 if (A.defer && lane < 6) {
-                    const int64_t nb = face_neighbour(v, lane, A.cps);
+                    nb = face_neighbour(v, lane, A.cps);
                     const uint32_t kv = __ldcg(&A.key[v]), sv = __ldcg(&A.state[v]), gv = __ldcg(&A.gen[v]);
                     uint32_t sn = 0, kn = KEY_INF, gn = 0;
                     if (nb >= 0) { sn = __ldcg(&A.state[nb]); kn = __ldcg(&A.key[nb]); gn = __ldcg(&A.gen[nb]); }
                     // mode 4: only neighbours across an inflow face of v matter
                     if (nb >= 0 && !(A.defer == 4 && !(sv & (1u << lane)))) {
-                        if (sn & ST_RUNNING) d = true;
+                        if (sn & ST_RUNNING) d = drun = true;
                         else if (sn & ST_QUEUED) {
                             if (A.defer == 5) d = gn < gv;
                             else if (A.defer == 2) d = kn < kv || (kn == kv && (uint32_t)nb < v);
@@ -1919,11 +1938,29 @@ k_async(CellArgs A)
                     }
                 }
                 if (__any_sync(0xffffffffu, d)) {
+                    // Deferred.  Blocked by a RUNNING neighbour: park on it -- set v's bit in the
+                    // neighbour's waiter word; its release re-queues v (no cycling through the
+                    // ring: a re-push goes behind every other deferred cell, and the critical
+                    // path waited a whole ring cycle per cell diagonal, ~30 us on C3).  Whoever
+                    // clears the bit pushes v, so v is queued exactly once: if the neighbour
+                    // stopped running before v's bit was set, v takes the bit back and re-pushes
+                    // itself (Dekker order: bit set, fence, state read / state cleared, fence,
+                    // waiter word taken).  Running cells never wait, so parking cannot deadlock.
+                    const unsigned rb = EIK_PARK ? __ballot_sync(0xffffffffu, drun) : 0u;
+                    const int fp = rb ? __ffs(rb) - 1 : 0;
+                    const int64_t nbp = __shfl_sync(0xffffffffu, nb, fp);
                     if (lane == 0) {
-                        const uint32_t slot = atomicAdd(&ctl->q_tail, 1u) & A.qmask;
-                        while (atomicCAS(&ring[slot], Q_EMPTY, v) != Q_EMPTY) __nanosleep(32);
+                        bool parked = false;
+                        if (rb) {
+                            const uint32_t bit = 1u << (fp ^ 1);   // face of nbp toward v
+                            atomicOr(&A.wait[nbp], bit);
+                            __threadfence();
+                            if (__ldcg(&A.state[nbp]) & ST_RUNNING) parked = true;
+                            else parked = !(atomicAnd(&A.wait[nbp], ~bit) & bit);   // the releaser took it
+                        }
+                        if (!parked) q_repush(ctl, ring, A.qmask, v);
                         atomicAdd(&ctl->defers, 1ull);
-                        __nanosleep(64);
+                        if (!parked) __nanosleep(64);
                     }
                     __syncwarp();
                     continue;
@@ -1984,6 +2021,18 @@ k_async(CellArgs A)
             }
             const uint32_t old = atomicAnd(&A.state[c], ~ST_RUNNING);
             if (old & ST_QUEUED) q_push(ctl, ring, A.qmask, c);   // tagged while running
+            if (EIK_PARK) {
+                // re-queue the neighbours parked on this cell (they stay counted in pending)
+                __threadfence();
+                uint32_t w = atomicExch(&A.wait[c], 0u);
+                while (w) {
+                    const int f = __ffs(w) - 1;
+                    w &= w - 1u;
+                    const int64_t nbw = face_neighbour(c, f, A.cps);
+                    EIK_CHECK(nbw >= 0 && nbw < (int64_t)A.cap, "parked neighbour");
+                    q_repush(ctl, ring, A.qmask, (uint32_t)nbw);
+                }
+            }
             const unsigned long long np = atomicAdd(&ctl->processings, 1ull) + 1ull;
             if (np > A.proc_limit) atomicExch(&ctl->abort, 1u);
             if (A.stats) {
@@ -2037,6 +2086,7 @@ k_dsweep(CellArgs A, int D)
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
     const int cps = A.cps;
+    if (ctl->err != 0u || ctl->n_exits == 0u) return;   // invalid input: no sweeping
     const uint32_t dir = ctl->sweep_idx & 7u;   // set by k_sweep_end (previous launch)
     const uint32_t beg = A.diag_off[D], end = A.diag_off[D + 1];
     T* Vt = reinterpret_cast<T*>(A.Vt);
@@ -2144,6 +2194,7 @@ k_dsweep(CellArgs A, int D)
 // seed the async ring with the initial cells (L <- Q^c, Alg. 1 line 2)
 __global__ void k_seed_queue(uint32_t* state, uint32_t* ring, Ctl* ctl, int64_t J)
 {
+    if (__ldcg(&ctl->err) != 0u || __ldcg(&ctl->n_exits) == 0u) return;   // invalid input: no work
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < J;
          base += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = base + threadIdx.x;
@@ -2159,8 +2210,11 @@ __global__ void k_seed_queue(uint32_t* state, uint32_t* ring, Ctl* ctl, int64_t 
 // A8: egress, tiles -> lexicographic U_out
 // --------------------------------------------------------------------------------------
 template <typename T>
-__global__ void k_egress(Geom g, const T* __restrict__ Vt, T* __restrict__ U, int64_t M)
+__global__ void k_egress(Geom g, const T* __restrict__ Vt, T* __restrict__ U, int64_t M, const Ctl* ctl)
 {
+    // a device-detected input error or an aborted loop leaves U_out untouched (EIK_EINVAL
+    // contract; the host reads the status once, after this kernel)
+    if (__ldcg(&ctl->err) != 0u || __ldcg(&ctl->abort) != 0u || __ldcg(&ctl->n_exits) == 0u) return;
     // four consecutive output points of one (j, k) row per thread, flat over the z-plane
     // (blockIdx.y strides over k): one 16-byte tile read, four coalesced scalar writes
     const int r = g.r, lr = g.lr;

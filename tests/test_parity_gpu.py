@@ -239,6 +239,14 @@ def test_einval_leaves_output_untouched(solver):
         q2[0] = val
         assert call(q_=q2) == eik.EIK_EINVAL
     assert call(m_=torch.zeros_like(m)) == eik.EIK_EINVAL     # no exit (R10)
+    # h/F out of the precision's supported range (hf^2 subnormal / 3 hf^2 overflowing)
+    F3 = F.clone()
+    F3[40] = 1e-300
+    assert call(F_=F3) == eik.EIK_EINVAL
+    F4 = F.float().clone()
+    F4[40] = 1e-25                                            # fp32: h/F = 1.25e24 > 2^60
+    assert call(F_=F4, q_=q.float(), prec=0) == eik.EIK_EINVAL
+    assert "range" in eik.lib.eik_last_error(solver._ctx).decode()
     assert bool((U == 7.0).all())
     # -0 exit value is canonicalised to +0
     q3 = q.clone()

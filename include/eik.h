@@ -67,9 +67,11 @@ typedef enum {
                                 2 ... or is queued with a smaller (key, index); 3 ... with a key
                                 smaller by > bin width; 4 as 2 across inflow faces only; 5 ...
                                 or is queued from an older activation generation; 6 ... or is
-                                queued with a smaller (generation, key, index) [6]; 7 ... with a
-                                smaller (key, generation, index).  2, 6 and 7 are strict total
-                                orders: the smallest queued cell is never deferred              */
+                                queued with a smaller (generation, key, index); 7 ... with a
+                                smaller (key, generation, index); 8 automatic: 6 until the solve
+                                has run more than 6 processings per processed cell, then 2 [8].
+                                2, 6 and 7 are strict total orders: the smallest queued cell is
+                                never deferred                                                  */
     EIK_OPT_MAX_SWEEPS = 6,  /* sweeps per cell processing before the cell saves its active
                                 points and re-queues itself (bounds the round length, which is
                                 the slowest cell's); 0 = until convergence; -1 = automatic: 4
@@ -88,9 +90,14 @@ typedef enum {
                                 1 = the legacy Eq. (4): V_max + D / F(y), never
                                 reset.  Orders work only (bin width < inf, async readiness);
                                 the fixed point is the same                          */
-    EIK_OPT_TRACE = 10       /* diagnostics, async mode: record up to this many cell processings
+    EIK_OPT_TRACE = 10,      /* diagnostics, async mode: record up to this many cell processings
                                 (cell, tagger, pop / swept / end times, sweeps, flags, generation)
                                 for eik_get_trace; 0 = off [0]                                  */
+    EIK_OPT_CELL_KERNEL = 11 /* cell-sweep kernel of the async scheduler for r = 16 (kappa = 0,
+                                no sweep cap): 1 = 2x2x2 micro-blocks, one thread per block and
+                                block activity flags [1]; 0 = one thread per point (the point
+                                wavefront used for every other configuration).  Same fixed
+                                point                                               */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */

@@ -22,7 +22,7 @@ EIK_F32, EIK_F64 = 0, 1
 EIK_DFSM, EIK_DLSM = 0, 1          # eik_solve_sweep methods
 (EIK_OPT_BIN_WIDTH, EIK_OPT_MAX_ROUNDS, EIK_OPT_LOOP_MODE, EIK_OPT_COLLECT_STATS,
  EIK_OPT_TIME_CELL_EVENTS, EIK_OPT_ASYNC_DEFER, EIK_OPT_MAX_SWEEPS, EIK_OPT_TIMEOUT_S, EIK_OPT_KAPPA, EIK_OPT_CELL_KEY,
- EIK_OPT_TRACE) = range(11)
+ EIK_OPT_TRACE, EIK_OPT_CELL_KERNEL) = range(12)
 STATUS_NAMES = {0: "EIK_OK", 1: "EIK_EINVAL", 2: "EIK_ENOMEM", 3: "EIK_ECUDA",
                 4: "EIK_ENOTSUP", 5: "EIK_EINTERNAL"}
 

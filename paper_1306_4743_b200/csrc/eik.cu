@@ -36,10 +36,12 @@ struct eik_ctx {
     int loop_mode = 0;            // asynchronous persistent scheduler (see include/eik.h)
     int collect_stats = 1;
     int time_cell_events = 0;
-    int async_defer = 6;
+    int async_defer = 8;
     int max_sweeps = -1;          // -1: automatic (0 in async mode, 4 in the round modes)
     double kappa = 0.0;
     int legacy_key = 0;
+    int cell_kernel = 0;          // EIK_OPT_CELL_KERNEL: 1 = 2x2x2 micro-blocks (r = 16), 0 = point wavefront
+    bool last_b2 = false;         // the last async solve ran the micro-block kernel
     double timeout_s = 120.0;
     uint32_t trace_cap = 0;       // EIK_OPT_TRACE: processings traced (0 = off)
     uint4* trace = nullptr;
@@ -68,6 +70,7 @@ struct eik_ctx {
     // plane tables per r (index 0: r=4, 1: r=8, 2: r=16)
     uint16_t* plane_tab[3] = {nullptr, nullptr, nullptr};
     uint32_t* tab16 = nullptr;    // r = 16 packed per-direction plane table (sweep16)
+    uint2* tab_b2 = nullptr;      // r = 16 per-direction block-plane table (eik_b2.cuh)
     // host-pointer staging (eik_solve_host)
     void* stage = nullptr;
     size_t stage_bytes = 0;
@@ -162,6 +165,33 @@ static void make_tab16(int nt, std::vector<uint32_t>& tab)
         }
 }
 
+// per-direction block-plane table of the micro-block kernel (eik_b2.cuh): plane S of the
+// reflected block coordinates (A', B', C') of direction d, thread t: the t-th block (canonical
+// order c, b) reflected into physical (A, B, C)
+static void make_tab_b2(std::vector<uint2>& tab)
+{
+    const int nb = B2::NB, nt = B2::NT, rows = B2::ROWS;
+    tab.assign((size_t)8 * rows * nt, make_uint2(B2_DUMMY_X, 0u));
+    for (int d = 0; d < 8; ++d)
+        for (int S = 0; S < B2::NBP; ++S) {
+            int t = 0;
+            for (int c = 0; c < nb; ++c)
+                for (int b = 0; b < nb; ++b) {
+                    const int a = S - b - c;
+                    if (a < 0 || a >= nb) continue;
+                    const int pa = (d & 1) ? nb - 1 - a : a, pb = (d & 2) ? nb - 1 - b : b,
+                              pc = (d & 4) ? nb - 1 - c : c;
+                    const uint32_t q0 = (uint32_t)b2q(2 * pa, 2 * pb, 2 * pc);
+                    const uint32_t eb = (uint32_t)(pa + nb * pb + nb * nb * pc);
+                    const uint32_t bm = (a < nb - 1 ? 1u : 0u) | (a > 0 ? 2u : 0u) | (b < nb - 1 ? 4u : 0u) |
+                                        (b > 0 ? 8u : 0u) | (c < nb - 1 ? 16u : 0u) | (c > 0 ? 32u : 0u);
+                    const uint32_t h0 = (uint32_t)(2 * pa + 16 * 2 * pb + 256 * 2 * pc);
+                    tab[((size_t)d * rows + S) * nt + t++] = make_uint2(q0 | (eb << 13) | (bm << 23), h0);
+                }
+            if (t > nt) std::abort();
+        }
+}
+
 extern "C" int eik_abi_version(void) { return EIK_ABI_VERSION; }
 
 extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
@@ -208,6 +238,16 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
         CK(cudaMalloc(&ctx->tab16, tab.size() * sizeof(uint32_t)));
         CK(cudaMemcpy(ctx->tab16, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
+    {
+        std::vector<uint2> tab;
+        make_tab_b2(tab);
+        CK(cudaMalloc(&ctx->tab_b2, tab.size() * sizeof(uint2)));
+        CK(cudaMemcpy(ctx->tab_b2, tab.data(), tab.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+    }
+    CK(cudaFuncSetAttribute(k_async<float, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2_smem_bytes<float>()));
+    CK(cudaFuncSetAttribute(k_async<double, 16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b2_smem_bytes<double>()));
+    CK(cudaFuncSetAttribute(k_async<float, 16, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaFuncSetAttribute(k_async<double, 16, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     // opt in to > 48 KB dynamic shared memory for the cell kernels
     CK(cudaFuncSetAttribute(k_cell<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<float, 16>()));
     // largest shared-memory carveout: the cell kernels are occupancy-limited by shared memory
@@ -271,6 +311,7 @@ extern "C" void eik_destroy(eik_ctx* ctx)
     cudaFreeHost(ctx->ctl_host);
     for (int t = 0; t < 3; ++t) cudaFree(ctx->plane_tab[t]);
     cudaFree(ctx->tab16);
+    cudaFree(ctx->tab_b2);
     for (int i = 0; i < 5; ++i) if (ctx->ev[i]) cudaEventDestroy(ctx->ev[i]);
     for (int i = 0; i < 2; ++i) if (ctx->cev[i]) cudaEventDestroy(ctx->cev[i]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -315,7 +356,7 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
         ctx->time_cell_events = value != 0;
         return EIK_OK;
     case EIK_OPT_ASYNC_DEFER:
-        if (value < 0 || value > 7) return fail(ctx, EIK_EINVAL, "defer mode must be 0..7");
+        if (value < 0 || value > 8) return fail(ctx, EIK_EINVAL, "defer mode must be 0..8");
         ctx->async_defer = (int)value;
         return EIK_OK;
     case EIK_OPT_KAPPA:
@@ -329,6 +370,10 @@ extern "C" int eik_set_option(eik_ctx* ctx, int option, double value)
     case EIK_OPT_TIMEOUT_S:
         if (!(value > 0)) return fail(ctx, EIK_EINVAL, "timeout must be > 0 s");
         ctx->timeout_s = value;
+        return EIK_OK;
+    case EIK_OPT_CELL_KERNEL:
+        if (value != 0 && value != 1) return fail(ctx, EIK_EINVAL, "cell kernel must be 0 or 1");
+        ctx->cell_kernel = (int)value;
         return EIK_OK;
     case EIK_OPT_TRACE:
         if (!(value >= 0) || value > 1e8) return fail(ctx, EIK_EINVAL, "trace capacity must be in [0, 1e8]");
@@ -475,10 +520,11 @@ __global__ void k_round_end_graph(Ctl* ctl, cudaGraphConditionalHandle h)
     cudaGraphSetConditional(h, round_end_body(ctl) ? 0u : 1u);
 }
 
-template <typename T, int R>
+template <typename T, int R, int MODE = 0>
 static int launch_async(eik_ctx* ctx, const CellArgs& a, int grid)
 {
-    k_async<T, R><<<grid, CellCfg<R>::NT, cell_smem_bytes<T, R>(), ctx->stream>>>(a);
+    if constexpr (MODE == 1) k_async<T, 16, 1><<<grid, B2::NT, b2_smem_bytes<T>(), ctx->stream>>>(a);
+    else k_async<T, R><<<grid, CellCfg<R>::NT, cell_smem_bytes<T, R>(), ctx->stream>>>(a);
     CK(cudaGetLastError());
     return EIK_OK;
 }
@@ -486,9 +532,12 @@ static int launch_async(eik_ctx* ctx, const CellArgs& a, int grid)
 template <typename T>
 static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
 {
+    // r = 16 exact path without a sweep cap: the 2x2x2 micro-block cell kernel (eik_b2.cuh)
+    const bool b2 = r == 16 && ctx->cell_kernel == 1 && ca.kappa == 0.0 && ca.max_sweeps == 0;
     int occ = 0;
     cudaError_t e;
-    if (r == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 16>, CellCfg<16>::NT, cell_smem_bytes<T, 16>());
+    if (b2) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 16, 1>, B2::NT, b2_smem_bytes<T>());
+    else if (r == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 16>, CellCfg<16>::NT, cell_smem_bytes<T, 16>());
     else if (r == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 8>, CellCfg<8>::NT, cell_smem_bytes<T, 8>());
     else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_async<T, 4>, CellCfg<4>::NT, cell_smem_bytes<T, 4>());
     CK(e);
@@ -496,6 +545,7 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
 #ifdef EIK_ASYNC_OCC_CAP
     if (occ > EIK_ASYNC_OCC_CAP) occ = EIK_ASYNC_OCC_CAP;   // (experiment: fewer CTAs per SM)
 #endif
+    ctx->last_b2 = b2;
     // every CTA is co-resident (grid = occupancy x SMs): idle CTAs only poll the ring
     const int grid = occ * ctx->sm_count;
     ca.qmask = (uint32_t)(ctx->ring_cap - 1);
@@ -523,7 +573,8 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     CK(cudaGetLastError());
     const bool te = ctx->time_cell_events != 0;   // CUDA events around the persistent launch
     if (te) CK(cudaEventRecord(ctx->cev[0], ctx->stream));
-    int st = r == 16 ? launch_async<T, 16>(ctx, ca, grid) : r == 8 ? launch_async<T, 8>(ctx, ca, grid)
+    int st = b2 ? launch_async<T, 16, 1>(ctx, ca, grid)
+           : r == 16 ? launch_async<T, 16>(ctx, ca, grid) : r == 8 ? launch_async<T, 8>(ctx, ca, grid)
                                                                  : launch_async<T, 4>(ctx, ca, grid);
     if (te) CK(cudaEventRecord(ctx->cev[1], ctx->stream));
     return st;
@@ -765,6 +816,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     init.t_start = ~0ull;
     init.budget_ns = (unsigned long long)(ctx->timeout_s * 1e9);
     init.kappa_f = (float)ctx->kappa;
+    init.auto_mode = 6u;
     ctx->ms_cell_events = 0;
     *ctx->ctl_host = init;
     CK(cudaEventRecord(ctx->ev[0], s));
@@ -798,6 +850,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     const int ri = rindex_of(r);
     ca.plane_tab = ctx->plane_tab[ri];
     ca.tab16 = ctx->tab16;
+    ca.tab_b2 = ctx->tab_b2;
     ca.Vt = ctx->Vt;
     ca.Ht = ctx->Ht;
     // automatic sweep cap: rounds last as long as their slowest processing, so the round modes

@@ -253,6 +253,8 @@ struct Ctl {
     uint32_t sweep_dmax;          // largest value change of the current sweep (float bits, up)
     float kappa_f;                // early termination threshold of the sweeps
     uint32_t trace_n;             // async mode processing trace (EIK_OPT_TRACE): entries written
+    uint32_t first_procs;         // async mode: cells processed at least once
+    uint32_t auto_mode;           // async readiness mode 8: the mode in force (6, then 2)
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -607,6 +609,7 @@ struct CellArgs {
     uint32_t* wait;              // async mode: bit f = the neighbour across face f is parked on this cell
     const uint16_t* plane_tab;   // [NPL + 3][NT] canonical point of thread t in plane s (0xFFFF: none)
     const uint32_t* tab16;       // r = 16: [8][NPL + 3][NT] packed per-direction plane table (sweep16)
+    const uint2* tab_b2;         // r = 16 micro-block kernel: [8][22 + 2][64] block-plane table (eik_b2.cuh)
     void* Vt;
     const void* Ht;
     int64_t n1;
@@ -902,6 +905,11 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
 // Against sweep_dir this removes the per-step coordinate arithmetic (box offset, reflection,
 // border tests) and the branches; the activations are predicated stores at compile-time
 // offsets.  kappa = 0 only (the exact path; kappa > 0 runs sweep_dir).
+// points per wavefront plane s = a + b + c of a 16^3 cell (warps past it skip the step)
+__constant__ uint8_t c_pcnt16[48] = {
+    1, 3, 6, 10, 15, 21, 28, 36, 45, 55, 66, 78, 91, 105, 120, 136, 150, 162, 172, 180, 186, 190,
+    192, 192, 190, 186, 180, 172, 162, 150, 136, 120, 105, 91, 78, 66, 55, 45, 36, 28, 21, 15, 10,
+    6, 3, 1, 0, 0};
 static constexpr uint32_t T16_DUMMY_P = 16 * 16 * 16 + 1;                       // act[R3 + 1]
 static constexpr uint32_t T16_DUMMY = (1u + 18u + 324u) | (T16_DUMMY_P << 19);   // box (-1, 0, 0)
 static constexpr int T16_ROWS = 3 * 16 - 2 + 3;   // NPL + 3 trailing empty planes
@@ -929,6 +937,7 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
     const uint32_t* __restrict__ tp = tab + DIR * T16_ROWS * NT + threadIdx.x;
     uint32_t one;
     asm("mov.u32 %0, 1;" : "=r"(one));
+    const uint32_t wbase = threadIdx.x & ~31u;   // first thread of this warp (points fill threads in order)
     bool fwd = false;
     uint32_t bwd = 0;
     int s = __ffsll((long long)pm) - 1;
@@ -959,6 +968,7 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
             const uint32_t ue = en;
             const T hs = hn;
             EIK16_PREFETCH()
+            if (c_pcnt16[s] <= wbase) { __syncthreads(); ++nsteps; continue; }   // no point in this warp
             const uint32_t qa = vb + (ue & 0x1fffu) * TS;
             const uint32_t fa = ab + (ue >> 19);
             const T v = lds<T>(qa);
@@ -1000,6 +1010,11 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
         const uint32_t ue = en;
         const T hs = hn;
         EIK16_PREFETCH()
+        if (c_pcnt16[s] <= wbase) {   // no point of plane s in this warp: only the barrier
+            fwd = __syncthreads_or(false);
+            ++nsteps;
+            continue;
+        }
         const uint32_t qa = vb + (ue & 0x1fffu) * TS;
         const uint32_t fa = ab + (ue >> 19);
         // flag and the seven box values in one shared-memory round trip
@@ -1847,7 +1862,10 @@ k_cell(CellArgs A)
 // __threadfence (the flush of P:686-688); readers take the cell with an atomic and read
 // tiles through L2 (.cg), so a stale read is only ever a valid upper bound and
 // is followed by a re-activation.
-enum : uint32_t { ST_QUEUED = 256u, ST_RUNNING = 512u, Q_EMPTY = 0xffffffffu };
+enum : uint32_t { ST_QUEUED = 256u, ST_RUNNING = 512u, ST_VISITED = 1024u, Q_EMPTY = 0xffffffffu };
+#ifndef EIK_AUTO_RATIO
+#define EIK_AUTO_RATIO 6ull   // readiness mode 8: switch to the key order above this processings / cell (measured: 4 slows P2 / P3 / C2d, 6 does not; PMAZE 84 -> 49 ms)
+#endif
 
 __device__ __forceinline__ void q_push(Ctl* ctl, uint32_t* ring, uint32_t qmask, uint32_t c)
 {
@@ -1867,19 +1885,33 @@ __device__ __forceinline__ void q_repush(Ctl* ctl, uint32_t* ring, uint32_t qmas
 #define EIK_PARK 0   // 1: a cell deferred by a running neighbour waits on it instead of cycling the ring (measured: C3 7.17 -> 7.57 ms, C5 35.7 -> 36.4; off)
 #endif
 
-template <typename T, int R>
-__global__ void __launch_bounds__(CellCfg<R>::NT, MinBlocks<T, R>::value)
+}  // namespace eik
+#include "eik_b2.cuh"
+namespace eik {
+
+// cell kernel of the async scheduler: MODE 0 = cell_process (point wavefront), MODE 1 = the
+// 2x2x2 micro-block form (r = 16 only, eik_b2.cuh)
+template <typename T, int R, int MODE> struct AsyncCfg {
+    static constexpr int NT = CellCfg<R>::NT;
+    static constexpr int MINB = MinBlocks<T, R>::value;
+};
+template <typename T> struct AsyncCfg<T, 16, 1> {
+    static constexpr int NT = B2::NT;
+    static constexpr int MINB = B2Minb<T>::value;
+};
+
+template <typename T, int R, int MODE = 0>
+__global__ void __launch_bounds__((AsyncCfg<T, R, MODE>::NT), (AsyncCfg<T, R, MODE>::MINB))
 k_async(CellArgs A)
 {
-    using C = CellCfg<R>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    CellSmem<T, R> Msm(smem_raw);
     __shared__ CellShared<R> S;
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
     uint32_t* ring = A.wl0;
     if (tid == 0) atomicMin(&ctl->t_start, gtimer());
     uint32_t tr_pid = 0, tr_tag = 0, tr_pop = 0, tr_swept = 0;   // processing trace (thread 0)
+    uint32_t gen_c = 0;                                          // generation of the cell (thread 0)
     for (;;) {
         if (tid < 32) {   // warp 0 pops the next cell; the other warps wait at the barrier
             const int lane = tid;
@@ -1918,21 +1950,24 @@ k_async(CellArgs A)
                 // and v is re-queued while a neighbour runs or is queued ahead of it
                 bool d = false, drun = false;
                 int64_t nb = -1;
-                if (A.defer && lane < 6) {
+                // mode 8 (automatic): mode 6 until the solve has run more than EIK_AUTO_RATIO
+                // processings per processed cell, then mode 2 for the rest (see release below)
+                const int dm = A.defer == 8 ? (int)__ldcg(&ctl->auto_mode) : A.defer;
+                if (dm && lane < 6) {
                     nb = face_neighbour(v, lane, A.cps);
                     const uint32_t kv = __ldcg(&A.key[v]), sv = __ldcg(&A.state[v]), gv = __ldcg(&A.gen[v]);
                     uint32_t sn = 0, kn = KEY_INF, gn = 0;
                     if (nb >= 0) { sn = __ldcg(&A.state[nb]); kn = __ldcg(&A.key[nb]); gn = __ldcg(&A.gen[nb]); }
                     // mode 4: only neighbours across an inflow face of v matter
-                    if (nb >= 0 && !(A.defer == 4 && !(sv & (1u << lane)))) {
+                    if (nb >= 0 && !(dm == 4 && !(sv & (1u << lane)))) {
                         if (sn & ST_RUNNING) d = drun = true;
                         else if (sn & ST_QUEUED) {
-                            if (A.defer == 5) d = gn < gv;
-                            else if (A.defer == 2) d = kn < kv || (kn == kv && (uint32_t)nb < v);
-                            else if (A.defer == 3) d = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
-                            else if (A.defer == 6)   // strict total order (no deferral cycles)
+                            if (dm == 5) d = gn < gv;
+                            else if (dm == 2) d = kn < kv || (kn == kv && (uint32_t)nb < v);
+                            else if (dm == 3) d = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
+                            else if (dm == 6)   // strict total order (no deferral cycles)
                                 d = gn < gv || (gn == gv && (kn < kv || (kn == kv && (uint32_t)nb < v)));
-                            else if (A.defer == 7)
+                            else if (dm == 7)
                                 d = kn < kv || (kn == kv && (gn < gv || (gn == gv && (uint32_t)nb < v)));
                         }
                     }
@@ -1970,7 +2005,10 @@ k_async(CellArgs A)
             }
             if (lane == 0) {
                 if (got != Q_EMPTY) {
-                    fl = atomicExch(&A.state[got], ST_RUNNING) & 255u;   // faces + INIT + CONT
+                    const uint32_t ost = atomicExch(&A.state[got], ST_RUNNING | ST_VISITED);
+                    fl = ost & 255u;                                        // faces + INIT + CONT
+                    if (!(ost & ST_VISITED)) atomicAdd(&ctl->first_procs, 1u);
+                    if (A.defer >= 5) gen_c = __ldcg(&A.gen[got]);   // (thread 0; broadcast at the tags)
                     if (!A.legacy_key) A.key[got] = KEY_INF;             // V^c <- +inf
                     // (no fence: the tile loads depend on `got`, which was read from the ring
                     // after its producer fenced the cell's values, and go to L2)
@@ -1990,9 +2028,18 @@ k_async(CellArgs A)
         if (c == Q_EMPTY) break;
         const long long t0 = clock64();
         unsigned long long nsw = 0;
-        cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
+        if constexpr (MODE == 1 && R == 16) {
+            B2Smem<T> Mb(smem_raw);
+            cell_process_b2<T>(A, S, Mb, c, S.flags, nsw);
+        } else {
+            CellSmem<T, R> Msm(smem_raw);
+            cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
+        }
         if (A.trace && tid == 0) tr_swept = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
-        if (tid < 32) tr_pid = __shfl_sync(0xffffffffu, tr_pid, 0);
+        if (tid < 32) {
+            tr_pid = __shfl_sync(0xffffffffu, tr_pid, 0);
+            gen_c = __shfl_sync(0xffffffffu, gen_c, 0);
+        }
         __threadfence();   // value stores before the re-activations
         __syncthreads();
         // re-activations first, then the cell's own release: a neighbour waiting for this
@@ -2002,7 +2049,7 @@ k_async(CellArgs A)
             const int64_t nc = face_neighbour(c, tid, A.cps);
             if (nc >= 0) {
                 atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
-                if (A.defer >= 5) atomicMax(&A.gen[nc], __ldcg(&A.gen[c]) + 1u);
+                if (A.defer >= 5) atomicMax(&A.gen[nc], gen_c + 1u);
                 if (A.trace) A.tagger[nc] = tr_pid;
                 const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
                 if (!(old & (ST_QUEUED | ST_RUNNING))) {
@@ -2035,6 +2082,13 @@ k_async(CellArgs A)
             }
             const unsigned long long np = atomicAdd(&ctl->processings, 1ull) + 1ull;
             if (np > A.proc_limit) atomicExch(&ctl->abort, 1u);
+            // automatic readiness (mode 8): the generation order keeps the front wide but re-runs
+            // cells whose true upwind neighbour arrives later through faster regions; once
+            // processings exceed EIK_AUTO_RATIO per processed cell (slow barriers, pinched level
+            // sets: P:1644-1648), the rest of the solve takes the key (heap) order of Alg. 3
+            if (A.defer == 8 && np > EIK_AUTO_RATIO * (unsigned long long)__ldcg(&ctl->first_procs) + 4096ull &&
+                __ldcg(&ctl->auto_mode) != 2u)
+                atomicExch(&ctl->auto_mode, 2u);
             if (A.stats) {
                 cell_stats<R>(A, S, c, nsw);
                 const unsigned long long cyc = (unsigned long long)(clock64() - t0);

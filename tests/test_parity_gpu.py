@@ -157,17 +157,19 @@ def test_host_path_pinned_exit_values_in_place(solver):
             solver.solve_host(Fp, mp, qb, cell_size=8, n=w.n)
 
 
-@pytest.mark.parametrize("mode,delta,msw,defer", [
-    (0, 0.0, 0, 1), (0, 0.0, 2, 1), (0, 0.0, 0, 0), (0, 0.0, 0, 2), (0, 0.05, 0, 3),
-    (1, 0.0, 0, 1), (1, 0.05, 0, 1), (1, 1e-6, 3, 1),
-    (2, 0.0, 0, 1), (2, 0.05, 1, 1), (2, 1e-6, 0, 1)])
-def test_schedule_independence(mode, delta, msw, defer):
-    """Loop mode, bin width, sweep cap (continuation) and async readiness rule change the work,
-    never the fixed point."""
+@pytest.mark.parametrize("mode,delta,msw,defer,kern", [
+    (0, 0.0, 0, 1, 1), (0, 0.0, 2, 1, 1), (0, 0.0, 0, 0, 1), (0, 0.0, 0, 2, 1), (0, 0.05, 0, 3, 1),
+    (0, 0.0, 0, 6, 0), (0, 0.0, 0, 0, 0), (0, 0.0, 0, 7, 1), (0, 0.0, 0, 6, 1),
+    (1, 0.0, 0, 1, 1), (1, 0.05, 0, 1, 1), (1, 1e-6, 3, 1, 1),
+    (2, 0.0, 0, 1, 1), (2, 0.05, 1, 1, 1), (2, 1e-6, 0, 1, 1)])
+def test_schedule_independence(mode, delta, msw, defer, kern):
+    """Loop mode, bin width, sweep cap (continuation), async readiness rule and the r = 16 cell
+    kernel (micro-block / point wavefront) change the work, never the fixed point."""
     import paper_1306_4743_b200 as eik
     s = eik.Solver(device=0, loop_mode=mode, bin_width=delta)
     s.set_option(eik.EIK_OPT_MAX_SWEEPS, msw)
     s.set_option(eik.EIK_OPT_ASYNC_DEFER, defer)
+    s.set_option(eik.EIK_OPT_CELL_KERNEL, kern)
     for w in (W.c2(48), W.c3(48), W.c4(48)):
         for r in (8, 16):
             for dt in (np.float64, np.float32):

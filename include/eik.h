@@ -198,7 +198,7 @@ int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n);
 /* Processing trace of the last solve (EIK_OPT_TRACE > 0, async mode): copies up to
  * max_entries entries of 8 uint32 each into out (host memory, 32 bytes per entry):
  *   {cell, id of the processing that last tagged it (0xFFFFFFFF: seeded), t_pop, t_swept,
- *    t_end, sweeps, state flags taken at the pop, activation generation}
+ *    t_end, sweeps, state flags taken at the pop, point writes}
  * with times in ns since the solve's start (t_swept: sweeps and write-back done, before the
  * neighbour tags; t_end: tags and release done).  The entry index is the processing id.
  * Returns the number of entries copied (0 if tracing is off), or -EIK_EINVAL / -EIK_ECUDA. */

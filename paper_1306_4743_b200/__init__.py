@@ -261,7 +261,7 @@ class Solver:
 
     def trace(self, max_entries: int = 1 << 26):
         """Processing trace of the last async solve (EIK_OPT_TRACE): numpy uint32 [n, 8] rows
-        {cell, tagger id, t_pop, t_swept, t_end, sweeps, flags, generation} (ns)."""
+        {cell, tagger id, t_pop, t_swept, t_end, sweeps, flags, writes} (ns)."""
         import numpy as np
         a = np.zeros((max_entries, 8), dtype=np.uint32)
         n = lib.eik_get_trace(self._ctx, a.ctypes.data, max_entries)

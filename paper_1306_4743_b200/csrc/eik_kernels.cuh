@@ -307,6 +307,9 @@ template <> struct Vec4T<double> { static __device__ __forceinline__ void st(dou
     const double2 x = __ldcg(reinterpret_cast<const double2*>(p)), y = __ldcg(reinterpret_cast<const double2*>(p) + 1);
     v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; } };
 
+#ifndef EIK_INGEST_U
+#define EIK_INGEST_U 4   // vectors of 4 points per thread and iteration (2: 61 % of HBM on C3)
+#endif
 template <typename T>
 __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __restrict__ mask,
                          const T* __restrict__ q, T* __restrict__ Vt, T* __restrict__ Ht,
@@ -325,18 +328,19 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
     const uint32_t np = cps << lr;             // padded points per side
     const uint32_t nvr = np >> 2;              // vectors per padded row
     const uint32_t nv = nvr * np;              // vectors per padded z-plane (< 2^32)
-    // two vectors per thread and iteration (t and t + S): eight loads of F and eight of the
+    // EIK_INGEST_U vectors per thread and iteration (t, t + S, ...): 4 U loads of F and of the
     // mask in flight before any is used
     const uint32_t S = gridDim.x * blockDim.x;
+    constexpr int U = EIK_INGEST_U;
     for (int64_t k = blockIdx.y; k < (int64_t)np; k += gridDim.y)
-    for (uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < nv; t0 += 2 * S) {
-        T f[2][4];
-        uint8_t mk[2][4];
-        int64_t i0[2], j[2], lex0[2], p0[2];
-        uint32_t c[2];
-        bool vin[2], row_in[2];
+    for (uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x; t0 < nv; t0 += U * S) {
+        T f[U][4];
+        uint8_t mk[U][4];
+        int64_t i0[U], j[U], lex0[U], p0[U];
+        uint32_t c[U];
+        bool vin[U], row_in[U];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             const uint32_t t = t0 + u * S;
             vin[u] = t < nv;
             const uint32_t j32 = t / nvr, iv = t - j32 * nvr;
@@ -355,7 +359,7 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
             }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < U; ++u) {
             if (!vin[u]) continue;
             const int a0 = (int)(i0[u] & (r - 1)), b = (int)(j[u] & (r - 1)), d = (int)(k & (r - 1));
             T vv[4], hh[4];
@@ -905,14 +909,54 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
 // Against sweep_dir this removes the per-step coordinate arithmetic (box offset, reflection,
 // border tests) and the branches; the activations are predicated stores at compile-time
 // offsets.  kappa = 0 only (the exact path; kappa > 0 runs sweep_dir).
-// points per wavefront plane s = a + b + c of a 16^3 cell (warps past it skip the step)
-__constant__ uint8_t c_pcnt16[48] = {
-    1, 3, 6, 10, 15, 21, 28, 36, 45, 55, 66, 78, 91, 105, 120, 136, 150, 162, 172, 180, 186, 190,
-    192, 192, 190, 186, 180, 172, 162, 150, 136, 120, 105, 91, 78, 66, 55, 45, 36, 28, 21, 15, 10,
-    6, 3, 1, 0, 0};
 static constexpr uint32_t T16_DUMMY_P = 16 * 16 * 16 + 1;                       // act[R3 + 1]
 static constexpr uint32_t T16_DUMMY = (1u + 18u + 324u) | (T16_DUMMY_P << 19);   // box (-1, 0, 0)
 static constexpr int T16_ROWS = 3 * 16 - 2 + 3;   // NPL + 3 trailing empty planes
+
+// Alg. 2 lines 8-13 for one updated point of sweep16, in PTX so that ptxas emits one
+// LOP3 (neighbour-exists bit -> predicate), one FSETP.AND and one predicated STS per neighbour:
+// for every neighbour that exists (bm bits 13-18: forward x, backward x, y, z) and holds a value
+// larger than u, set its activity byte.  Returns the forward activations (bit 0) and the
+// backward axes (bits 1-3).
+template <typename T, int OXP, int OYP, int OZP, bool FWD> struct Act16;
+#define EIK_ACT16_BODY(FT, CT)                                                                       \
+    static __device__ __forceinline__ uint32_t run(uint32_t bm, T xf, T xb, T yf, T yb, T zf, T zb,  \
+                                                   T u, uint32_t fa, uint32_t one)                  \
+    {                                                                                                \
+        uint32_t r;                                                                                  \
+        asm volatile("{\n\t.reg .pred q, p0, p1, p2, p3, p4, p5, pf;\n\t.reg .b32 t, a, b;\n\t"     \
+                     "and.b32 t, %1, 0x2000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p0, %2, %8, q;\n\t" \
+                     "and.b32 t, %1, 0x4000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p1, %3, %8, q;\n\t" \
+                     "and.b32 t, %1, 0x8000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p2, %4, %8, q;\n\t" \
+                     "and.b32 t, %1, 0x10000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p3, %5, %8, q;\n\t" \
+                     "and.b32 t, %1, 0x20000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p4, %6, %8, q;\n\t" \
+                     "and.b32 t, %1, 0x40000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p5, %7, %8, q;\n\t" \
+                     "@p0 st.shared.u8 [%9+%11], %10;\n\t@p1 st.shared.u8 [%9+%12], %10;\n\t"            \
+                     "@p2 st.shared.u8 [%9+%13], %10;\n\t@p3 st.shared.u8 [%9+%14], %10;\n\t"            \
+                     "@p4 st.shared.u8 [%9+%15], %10;\n\t@p5 st.shared.u8 [%9+%16], %10;\n\t"            \
+                     "or.pred pf, p0, p2;\n\tor.pred pf, pf, p4;\n\t"                                  \
+                     "selp.u32 t, 1, 0, pf;\n\tselp.u32 a, 2, 0, p1;\n\tselp.u32 b, 4, 0, p3;\n\t"      \
+                     "or.b32 t, t, a;\n\tor.b32 t, t, b;\n\tselp.u32 a, 8, 0, p5;\n\tor.b32 %0, t, a;\n\t}" \
+                     : "=r"(r)                                                                       \
+                     : "r"(FWD ? bm : (bm & 0x54000u)), CT(xf), CT(xb), CT(yf), CT(yb), CT(zf), CT(zb),  \
+                       CT(u), "r"(fa), "r"(one), "n"(OXP), "n"(-OXP), "n"(OYP), "n"(-OYP), "n"(OZP),   \
+                       "n"(-OZP)                                                                     \
+                     : "memory");                                                                    \
+        return r;                                                                                    \
+    }
+template <int OXP, int OYP, int OZP, bool FWD> struct Act16<float, OXP, OYP, OZP, FWD> {
+    using T = float;
+#define EIK_CF(x) "f"(x)
+    EIK_ACT16_BODY("f32", EIK_CF)
+#undef EIK_CF
+};
+template <int OXP, int OYP, int OZP, bool FWD> struct Act16<double, OXP, OYP, OZP, FWD> {
+    using T = double;
+#define EIK_CD(x) "d"(x)
+    EIK_ACT16_BODY("f64", EIK_CD)
+#undef EIK_CD
+};
+#undef EIK_ACT16_BODY
 
 template <typename T, int DIR>
 __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* __restrict__ tab,
@@ -928,7 +972,6 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
     // (unsigned: address arithmetic wraps modulo 2^32, a negative offset subtracts)
     constexpr uint32_t oxq = (uint32_t)(sx * TS), oyq = (uint32_t)(sy * C::RP * TS),
                        ozq = (uint32_t)(sz * C::RP2 * TS);                              // box bytes
-    constexpr uint32_t oxp = (uint32_t)sx, oyp = (uint32_t)(sy * 16), ozp = (uint32_t)(sz * 256);   // flag bytes
     const T INF = dinf<T>();
     const uint32_t vb = smem_u32(M.V);
     const uint32_t hb = HG ? 0u : smem_u32(M.H);
@@ -937,7 +980,6 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
     const uint32_t* __restrict__ tp = tab + DIR * T16_ROWS * NT + threadIdx.x;
     uint32_t one;
     asm("mov.u32 %0, 1;" : "=r"(one));
-    const uint32_t wbase = threadIdx.x & ~31u;   // first thread of this warp (points fill threads in order)
     bool fwd = false;
     uint32_t bwd = 0;
     int s = __ffsll((long long)pm) - 1;
@@ -968,7 +1010,6 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
             const uint32_t ue = en;
             const T hs = hn;
             EIK16_PREFETCH()
-            if (c_pcnt16[s] <= wbase) { __syncthreads(); ++nsteps; continue; }   // no point in this warp
             const uint32_t qa = vb + (ue & 0x1fffu) * TS;
             const uint32_t fa = ab + (ue >> 19);
             const T v = lds<T>(qa);
@@ -988,13 +1029,10 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
                     sts(qa, u);
                     EIK16_MARK(ue, hf)
                 }
-                const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
-                const bool bxa = (bm & (2u << 13)) && xb > u, bya = (bm & (8u << 13)) && yb > u,
-                           bza = (bm & (32u << 13)) && zb > u;
-                if (bxa) sts_u8(fa - oxp, one);
-                if (bya) sts_u8(fa - oyp, one);
-                if (bza) sts_u8(fa - ozp, one);
-                bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
+                // backward activations only (forward neighbours are visited later in this sweep)
+                const uint32_t ar = Act16<T, (int)sx, 16 * sy, 256 * sz, false>::run(
+                    chg ? ue : 0u, xf, xb, yf, yb, zf, zb, u, fa, one);
+                bwd |= ar >> 1;
             }
             __syncthreads();
             ++nsteps;
@@ -1010,11 +1048,6 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
         const uint32_t ue = en;
         const T hs = hn;
         EIK16_PREFETCH()
-        if (c_pcnt16[s] <= wbase) {   // no point of plane s in this warp: only the barrier
-            fwd = __syncthreads_or(false);
-            ++nsteps;
-            continue;
-        }
         const uint32_t qa = vb + (ue & 0x1fffu) * TS;
         const uint32_t fa = ab + (ue >> 19);
         // flag and the seven box values in one shared-memory round trip
@@ -1039,18 +1072,10 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
             }
             // lines 8-13: activate larger in-cell neighbours (the cross-border "currently
             // downwind" test is done once per processing)
-            const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
-            const bool fxa = (bm & (1u << 13)) && xf > u, bxa = (bm & (2u << 13)) && xb > u;
-            const bool fya = (bm & (4u << 13)) && yf > u, bya = (bm & (8u << 13)) && yb > u;
-            const bool fza = (bm & (16u << 13)) && zf > u, bza = (bm & (32u << 13)) && zb > u;
-            if (fxa) sts_u8(fa + oxp, one);
-            if (bxa) sts_u8(fa - oxp, one);
-            if (fya) sts_u8(fa + oyp, one);
-            if (bya) sts_u8(fa - oyp, one);
-            if (fza) sts_u8(fa + ozp, one);
-            if (bza) sts_u8(fa - ozp, one);
-            myfwd = fxa | fya | fza;
-            bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
+            const uint32_t ar = Act16<T, (int)sx, 16 * sy, 256 * sz, true>::run(
+                chg ? ue : 0u, xf, xb, yf, yb, zf, zb, u, fa, one);
+            myfwd = ar & 1u;
+            bwd |= ar >> 1;
         }
         fwd = __syncthreads_or(myfwd);
         ++nsteps;
@@ -2099,7 +2124,7 @@ k_async(CellArgs A)
             if (A.trace && tr_pid < A.trace_cap) {
                 const uint32_t te = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
                 A.trace[2 * tr_pid] = make_uint4(c, tr_tag, tr_pop, tr_swept);
-                A.trace[2 * tr_pid + 1] = make_uint4(te, (uint32_t)nsw, S.flags, __ldcg(&A.gen[c]));
+                A.trace[2 * tr_pid + 1] = make_uint4(te, (uint32_t)nsw, S.flags, (uint32_t)S.stat[1]);
             }
             __threadfence();
             atomicSub(&ctl->pending, 1u);

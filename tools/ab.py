@@ -28,6 +28,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
         print(json.dumps({"cfg": name, "lib": os.path.basename(eik.LIB_PATH), "ms": sum(ts) / len(ts),
                           "ms_min": min(ts), "proc": st["cell_processings"], "rounds": st["rounds"],
                           "upd_pt": st["point_updates"] / st["M"],
+                          "ms_ingest": st["ms_ingest"], "ms_loop": st["ms_loop"], "ms_egress": st["ms_egress"],
+                          "ms_cell": st["ms_cell_device"],
                           "csum": float(U[torch.isfinite(U)].double().sum())}), flush=True)
         s.close()
         del F, m, q, U

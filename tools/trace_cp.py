@@ -36,7 +36,7 @@ for name in args or ["C3"]:
     st = s.stats()
     tr = s.trace().astype(np.int64)
     s.close()
-    cell, tag, tpop, tsw, tend, nsw, fl, gen = tr.T
+    cell, tag, tpop, tsw, tend, nsw, fl, wr = tr.T
     N = len(tr)
     NONE = 0xFFFFFFFF
     # critical path
@@ -82,7 +82,11 @@ for name in args or ["C3"]:
            "path_start_us": float(tpop[p[0]]) / 1e3,
            "path_sweeps_mean": float(nsw[p].mean()), "all_sweeps_mean": float(nsw.mean()),
            "in_flight_per_40th": occ,
-           "path_gen_last": int(gen[p[-1]])}
+           "writes_pct_10_50_90": [float(x) for x in np.percentile(wr, [10, 50, 90])],
+           "procs_writes_lt64": float((wr < 64).mean()), "procs_writes_lt512": float((wr < 512).mean()),
+           "ctatime_share_writes_lt64": float(((tend - tpop) * (wr < 64)).sum() / (tend - tpop).sum()),
+           "ctatime_share_writes_lt512": float(((tend - tpop) * (wr < 512)).sum() / (tend - tpop).sum()),
+           "reproc_writes_median": float(np.median(wr[~is_first])) if (~is_first).any() else 0.0}
     print(json.dumps(out), flush=True)
     np.save(f"gpurun_out/trace_{name}.npy", tr)
     del F, m, q, U

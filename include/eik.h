@@ -200,7 +200,7 @@ int eik_get_debug(const eik_ctx* ctx, uint64_t* out, int n);
  *   {cell, id of the processing that last tagged it (0xFFFFFFFF: seeded), t_pop, t_swept,
  *    t_end, sweeps, state flags taken at the pop, point writes}
  * with times in ns since the solve's start (t_swept: sweeps and write-back done, before the
- * neighbour tags; t_end: tags and release done).  The entry index is the processing id.
+ * neighbour tags; t_end: tags done).  The entry index is the processing id.
  * Returns the number of entries copied (0 if tracing is off), or -EIK_EINVAL / -EIK_ECUDA. */
 int64_t eik_get_trace(const eik_ctx* ctx, uint32_t* out, int64_t max_entries);
 

@@ -826,8 +826,7 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     Geom g{n1, cps, r, r == 4 ? 2 : r == 8 ? 3 : 4};
     {
         const int64_t np = (int64_t)cps * r, nv = (np / 4) * np;   // vectors per padded z-plane
-        const int64_t per = 256 * EIK_INGEST_U;                      // vectors per block and iteration
-        const int bx = (int)((nv + per - 1) / per < 1024 ? (nv + per - 1) / per : 1024);
+        const int bx = (int)((nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64);
         const int by = (int)(np < 65535 ? np : 65535);
         k_ingest<T><<<dim3(bx, by), 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt,
                                                  (T*)ctx->Ht, ctx->key, ctx->state, ctx->ctl, P);

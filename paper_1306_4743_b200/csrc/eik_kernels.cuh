@@ -308,7 +308,7 @@ template <> struct Vec4T<double> { static __device__ __forceinline__ void st(dou
     v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; } };
 
 #ifndef EIK_INGEST_U
-#define EIK_INGEST_U 4   // vectors of 4 points per thread and iteration (2: 61 % of HBM on C3)
+#define EIK_INGEST_U 2   // vectors of 4 points per thread and iteration (4 measured slower: C3 0.52 -> 0.65 ms)
 #endif
 template <typename T>
 __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __restrict__ mask,
@@ -556,6 +556,9 @@ template <int R> struct CellCfg {
 #endif
 #ifndef EIK_PARITY
 #define EIK_PARITY 1
+#endif
+#ifndef EIK_STAGE_B32
+#define EIK_STAGE_B32 3   // fp32 tile vectors in flight per thread while staging (6: all of them, spills at 64 registers)
 #endif
 #ifndef EIK_SWEEP16
 #define EIK_SWEEP16 1   // r = 16, kappa = 0: the packed-table wavefront step (sweep16)
@@ -1040,14 +1043,12 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
         pmr = 0;
     }
     for (; s < NPL; ++s, pmr >>= 1) {
-        if (!(((uint32_t)pmr & 1u) | (uint32_t)fwd)) {
-            if (pmr == 0ull) break;
-            EIK16_PREFETCH()
-            continue;
-        }
+        const bool go = ((uint32_t)pmr & 1u) | (uint32_t)fwd;   // (CTA-uniform)
+        if (!go && pmr == 0ull) break;
         const uint32_t ue = en;
         const T hs = hn;
         EIK16_PREFETCH()
+        if (!go) continue;   // plane without active points: no step, no barrier
         const uint32_t qa = vb + (ue & 0x1fffu) * TS;
         const uint32_t fa = ab + (ue >> 19);
         // flag and the seven box values in one shared-memory round trip
@@ -1266,7 +1267,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         constexpr int EL = 16 / sizeof(T);                // elements per vector
         constexpr int NV = R3 / EL;                       // vectors per tile
         constexpr int PV = (NV + NT - 1) / NT;            // vectors per thread
-        constexpr int B = sizeof(T) == 4 ? 3 : 2;           // batch (register budget)
+        constexpr int B = sizeof(T) == 4 ? EIK_STAGE_B32 : 2;   // batch (register budget)
         const V4* Vt4 = reinterpret_cast<const V4*>(Vt + base);
         if constexpr (CellSmem<T, R>::HG) {
             M.Hg = Ht + base;
@@ -1738,17 +1739,26 @@ __device__ __forceinline__ int64_t face_neighbour(uint32_t c, int f, int cps)
 }
 
 template <int R>
+__device__ __forceinline__ void cell_stats_v(const CellArgs& A, unsigned long long st0, unsigned long long st1,
+                                             unsigned long long st2, uint32_t c, unsigned long long nsweeps);
+template <int R>
 __device__ __forceinline__ void cell_stats(const CellArgs& A, CellShared<R>& S, uint32_t c,
                                            unsigned long long nsweeps)
+{
+    cell_stats_v<R>(A, S.stat[0], S.stat[1], S.stat[2], c, nsweeps);
+}
+template <int R>
+__device__ __forceinline__ void cell_stats_v(const CellArgs& A, unsigned long long st0, unsigned long long st1,
+                                             unsigned long long st2, uint32_t c, unsigned long long nsweeps)
 {
     Ctl* ctl = A.ctl;
     const int cps = A.cps;
     const int64_t n1 = A.n1;
     const int cx = (int)(c % (uint32_t)cps), cy = (int)((c / (uint32_t)cps) % (uint32_t)cps),
               cz = (int)(c / ((uint32_t)cps * (uint32_t)cps));
-    atomicAdd(&ctl->updates, S.stat[0]);
-    atomicAdd(&ctl->writes, S.stat[1]);
-    atomicAdd(&ctl->bytes_written, S.stat[2]);
+    atomicAdd(&ctl->updates, st0);
+    atomicAdd(&ctl->writes, st1);
+    atomicAdd(&ctl->bytes_written, st2);
     atomicAdd(&ctl->sweeps, nsweeps);
     const int64_t rx = (n1 - (int64_t)cx * R) < R ? (n1 - (int64_t)cx * R) : R;
     const int64_t ry = (n1 - (int64_t)cy * R) < R ? (n1 - (int64_t)cy * R) : R;
@@ -1929,6 +1939,7 @@ template <typename T, int R, int MODE = 0>
 __global__ void __launch_bounds__((AsyncCfg<T, R, MODE>::NT), (AsyncCfg<T, R, MODE>::MINB))
 k_async(CellArgs A)
 {
+    constexpr int NTH = AsyncCfg<T, R, MODE>::NT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CellShared<R> S;
     const int tid = threadIdx.x;
@@ -2067,28 +2078,19 @@ k_async(CellArgs A)
         }
         __threadfence();   // value stores before the re-activations
         __syncthreads();
-        // re-activations first, then the cell's own release: a neighbour waiting for this
-        // cell to stop running must find its tag already set (releasing first let it run
-        // without the tag and then again with it: 50 % more processings on C4)
-        if (tid < 6 && (S.face_flag & (1u << tid))) {
-            const int64_t nc = face_neighbour(c, tid, A.cps);
-            if (nc >= 0) {
-                atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
-                if (A.defer >= 5) atomicMax(&A.gen[nc], gen_c + 1u);
-                if (A.trace) A.tagger[nc] = tr_pid;
-                const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
-                if (!(old & (ST_QUEUED | ST_RUNNING))) {
-                    q_push(ctl, ring, A.qmask, (uint32_t)nc);
-                    __threadfence();   // the push's pending increment before this cell's decrement
-                }
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
-            if (S.cont) {   // sweep cap: save the direction state, continue later
-                __stcg(&A.pdir[c], S.dstate);
+        // Re-activations first, then the cell's own release: a neighbour waiting for this cell
+        // to stop running must find its tag already set (releasing first let it run without
+        // the tag and then again with it: 50 % more processings on C4).  Warp 0 tags and then
+        // pops the next cell while thread 32 releases this one (its atomics overlap the pop):
+        // named barrier 1 = thread 32 has copied this processing's shared results, barrier 2 =
+        // the tags are out.
+        // the release of this cell by one thread (counters by value: S may be overwritten)
+        auto release = [&](uint32_t cont, uint32_t dstate, uint32_t cont_key, unsigned long long st0,
+                           unsigned long long st1, unsigned long long st2) {
+            if (cont) {   // sweep cap: save the direction state, continue later
+                __stcg(&A.pdir[c], dstate);
                 __threadfence();   // before the cell is re-queued below
-                atomicMin(&A.key[c], S.cont_key);
+                atomicMin(&A.key[c], cont_key);
                 atomicOr(&A.state[c], FLAG_CONT | ST_QUEUED);
             }
             const uint32_t old = atomicAnd(&A.state[c], ~ST_RUNNING);
@@ -2115,19 +2117,45 @@ k_async(CellArgs A)
                 __ldcg(&ctl->auto_mode) != 2u)
                 atomicExch(&ctl->auto_mode, 2u);
             if (A.stats) {
-                cell_stats<R>(A, S, c, nsw);
+                cell_stats_v<R>(A, st0, st1, st2, c, nsw);
                 const unsigned long long cyc = (unsigned long long)(clock64() - t0);
                 atomicAdd(&ctl->dbg[0], cyc);
                 atomicMax(&ctl->dbg[1], cyc);
                 atomicAdd(&ctl->dbg[3], 1ull);
             }
-            if (A.trace && tr_pid < A.trace_cap) {
+            __threadfence();
+            atomicSub(&ctl->pending, 1u);
+        };
+        if (tid < 32) {
+            if (tid < 6 && (S.face_flag & (1u << tid))) {
+                const int64_t nc = face_neighbour(c, tid, A.cps);
+                if (nc >= 0) {
+                    atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
+                    if (A.defer >= 5) atomicMax(&A.gen[nc], gen_c + 1u);
+                    if (A.trace) A.tagger[nc] = tr_pid;
+                    const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);
+                    if (!(old & (ST_QUEUED | ST_RUNNING))) {
+                        q_push(ctl, ring, A.qmask, (uint32_t)nc);
+                        __threadfence();   // the push's pending increment before this cell's decrement
+                    }
+                }
+            }
+            __syncwarp();
+            if constexpr (NTH >= 64) asm volatile("bar.arrive 2, 64;" ::: "memory");
+            if (tid == 0 && A.trace && tr_pid < A.trace_cap) {
                 const uint32_t te = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
                 A.trace[2 * tr_pid] = make_uint4(c, tr_tag, tr_pop, tr_swept);
                 A.trace[2 * tr_pid + 1] = make_uint4(te, (uint32_t)nsw, S.flags, (uint32_t)S.stat[1]);
             }
-            __threadfence();
-            atomicSub(&ctl->pending, 1u);
+            if constexpr (NTH >= 64) asm volatile("bar.sync 1, 64;" ::: "memory");   // S may be overwritten now
+            else if (tid == 0) release(S.cont, S.dstate, S.cont_key, S.stat[0], S.stat[1], S.stat[2]);
+        } else if (NTH >= 64 && tid < 64) {
+            // this processing's shared results, before warp 0's pop overwrites them
+            const uint32_t cont = S.cont, dstate = S.dstate, cont_key = S.cont_key;
+            const unsigned long long st0 = S.stat[0], st1 = S.stat[1], st2 = S.stat[2];
+            asm volatile("bar.arrive 1, 64;" ::: "memory");
+            asm volatile("bar.sync 2, 64;" ::: "memory");   // tags out
+            if (tid == 32) release(cont, dstate, cont_key, st0, st1, st2);
         }
     }
     if (tid == 0) atomicMax(&ctl->t_end, gtimer());

@@ -557,6 +557,12 @@ template <int R> struct CellCfg {
 #ifndef EIK_PARITY
 #define EIK_PARITY 1
 #endif
+#ifndef EIK_ACT_PTX
+#define EIK_ACT_PTX 0   // 1: activations as one PTX block (fewer SASS instructions, measured C5 31 -> 37 ms)
+#endif
+#ifndef EIK_ACT_CLOBBER
+#define EIK_ACT_CLOBBER : "memory"
+#endif
 #ifndef EIK_STAGE_B32
 #define EIK_STAGE_B32 3   // fp32 tile vectors in flight per thread while staging (6: all of them, spills at 64 registers)
 #endif
@@ -901,6 +907,26 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
     return bwd;
 }
 
+// L2 cache-eviction policy "evict last" and a read-only load with it (fp64 hf in global memory)
+__device__ __forceinline__ unsigned long long l2_evict_last_policy()
+{
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ldg_keep(const double* a, unsigned long long pol)
+{
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldg_keep(const float* a, unsigned long long pol)
+{
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
 // ---- r = 16 wavefront sweep with a packed per-direction plane table -------------------------
 // tab16[d][s][t] (built on the host, eik.cu make_tab16) describes the t-th point of plane s of
 // direction d: bits 0-12 its box index q = (a+1) + 18 (b+1) + 324 (c+1), bits 13-18 the
@@ -944,7 +970,7 @@ template <typename T, int OXP, int OYP, int OZP, bool FWD> struct Act16;
                      : "r"(FWD ? bm : (bm & 0x54000u)), CT(xf), CT(xb), CT(yf), CT(yb), CT(zf), CT(zb),  \
                        CT(u), "r"(fa), "r"(one), "n"(OXP), "n"(-OXP), "n"(OYP), "n"(-OYP), "n"(OZP),   \
                        "n"(-OZP)                                                                     \
-                     : "memory");                                                                    \
+                     EIK_ACT_CLOBBER);                                                               \
         return r;                                                                                    \
     }
 template <int OXP, int OYP, int OZP, bool FWD> struct Act16<float, OXP, OYP, OZP, FWD> {
@@ -983,6 +1009,9 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
     const uint32_t* __restrict__ tp = tab + DIR * T16_ROWS * NT + threadIdx.x;
     uint32_t one;
     asm("mov.u32 %0, 1;" : "=r"(one));
+    // HG (fp64): the cell's hf tile is read once per sweep through L2; an evict_last policy keeps
+    // it there between the sweeps of a processing instead of re-fetching it from HBM
+    const unsigned long long l2keep = HG ? l2_evict_last_policy() : 0ull;
     bool fwd = false;
     uint32_t bwd = 0;
     int s = __ffsll((long long)pm) - 1;
@@ -990,7 +1019,7 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
     uint32_t en = __ldg(tp + s * NT);
     uint32_t en1 = __ldg(tp + (s + 1) * NT);
     tp += (s + 2) * NT;
-#define EIK16_HF(e_) (HG ? (((e_) >> 19) < (uint32_t)R3 ? __ldg(hg + ((e_) >> 19)) : INF)          \
+#define EIK16_HF(e_) (HG ? (((e_) >> 19) < (uint32_t)R3 ? ldg_keep(hg + ((e_) >> 19), l2keep) : INF)   \
                          : lds<T>(hb + ((e_) >> 19) * TS))
     T hn = EIK16_HF(en);
 #define EIK16_PREFETCH()                                                                   \
@@ -1033,9 +1062,19 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
                     EIK16_MARK(ue, hf)
                 }
                 // backward activations only (forward neighbours are visited later in this sweep)
+#if EIK_ACT_PTX
                 const uint32_t ar = Act16<T, (int)sx, 16 * sy, 256 * sz, false>::run(
                     chg ? ue : 0u, xf, xb, yf, yb, zf, zb, u, fa, one);
                 bwd |= ar >> 1;
+#else
+                const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
+                const bool bxa = (bm & (2u << 13)) && xb > u, bya = (bm & (8u << 13)) && yb > u,
+                           bza = (bm & (32u << 13)) && zb > u;
+                if (bxa) sts_u8(fa - (uint32_t)sx, one);
+                if (bya) sts_u8(fa - (uint32_t)(16 * sy), one);
+                if (bza) sts_u8(fa - (uint32_t)(256 * sz), one);
+                bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
+#endif
             }
             __syncthreads();
             ++nsteps;
@@ -1073,10 +1112,25 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
             }
             // lines 8-13: activate larger in-cell neighbours (the cross-border "currently
             // downwind" test is done once per processing)
+#if EIK_ACT_PTX
             const uint32_t ar = Act16<T, (int)sx, 16 * sy, 256 * sz, true>::run(
                 chg ? ue : 0u, xf, xb, yf, yb, zf, zb, u, fa, one);
             myfwd = ar & 1u;
             bwd |= ar >> 1;
+#else
+            const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
+            const bool fxa = (bm & (1u << 13)) && xf > u, bxa = (bm & (2u << 13)) && xb > u;
+            const bool fya = (bm & (4u << 13)) && yf > u, bya = (bm & (8u << 13)) && yb > u;
+            const bool fza = (bm & (16u << 13)) && zf > u, bza = (bm & (32u << 13)) && zb > u;
+            if (fxa) sts_u8(fa + (uint32_t)sx, one);
+            if (bxa) sts_u8(fa - (uint32_t)sx, one);
+            if (fya) sts_u8(fa + (uint32_t)(16 * sy), one);
+            if (bya) sts_u8(fa - (uint32_t)(16 * sy), one);
+            if (fza) sts_u8(fa + (uint32_t)(256 * sz), one);
+            if (bza) sts_u8(fa - (uint32_t)(256 * sz), one);
+            myfwd = fxa | fya | fza;
+            bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
+#endif
         }
         fwd = __syncthreads_or(myfwd);
         ++nsteps;

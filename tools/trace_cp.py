@@ -71,7 +71,7 @@ for name in args or ["C3"]:
         lo, hi = bins[k], bins[k + 1]
         ov = np.clip(np.minimum(tend, hi) - np.maximum(tpop, lo), 0, None).sum() / (hi - lo)
         occ.append(round(float(ov), 1))
-    out = {"cfg": name, "ms_total": st["ms_total"], "ms_cell": st["ms_cell_device"], "processings": N,
+    out = {"cfg": name, "tag": os.environ.get("TRACE_TAG", ""), "opts": opts, "ms_total": st["ms_total"], "ms_cell": st["ms_cell_device"], "processings": N,
            "T_last_end_us": T / 1e3, "path_len": len(path),
            "path_first_frac": float(is_first[p].mean()),
            "path_wait_us": float(wait.sum()) / 1e3, "path_work_us": float(work.sum()) / 1e3,
@@ -88,6 +88,6 @@ for name in args or ["C3"]:
            "ctatime_share_writes_lt512": float(((tend - tpop) * (wr < 512)).sum() / (tend - tpop).sum()),
            "reproc_writes_median": float(np.median(wr[~is_first])) if (~is_first).any() else 0.0}
     print(json.dumps(out), flush=True)
-    np.save(f"gpurun_out/trace_{name}.npy", tr)
+    np.save(f"gpurun_out/trace_{name}{os.environ.get('TRACE_TAG', '')}.npy", tr)
     del F, m, q, U
     torch.cuda.empty_cache()

@@ -157,9 +157,7 @@ static void make_tab16(int nt, std::vector<uint32_t>& tab)
                               pc = (d & 4) ? r - 1 - c : c;
                     const uint32_t q = (uint32_t)((pa + 1) + (r + 2) * (pb + 1) + (r + 2) * (r + 2) * (pc + 1));
                     const uint32_t p = (uint32_t)(pa + r * pb + r * r * pc);
-                    const uint32_t bm = (a < r - 1 ? 1u : 0u) | (a > 0 ? 2u : 0u) | (b < r - 1 ? 4u : 0u) |
-                                        (b > 0 ? 8u : 0u) | (c < r - 1 ? 16u : 0u) | (c > 0 ? 32u : 0u);
-                    tab[((size_t)d * rows + s) * nt + t++] = q | (bm << 13) | (p << 19);
+                    tab[((size_t)d * rows + s) * nt + t++] = q | (p << 19);
                 }
             if (t > nt) std::abort();
         }

@@ -255,6 +255,7 @@ struct Ctl {
     uint32_t trace_n;             // async mode processing trace (EIK_OPT_TRACE): entries written
     uint32_t first_procs;         // async mode: cells processed at least once
     uint32_t auto_mode;           // async readiness mode 8: the mode in force (6, then 2)
+    uint32_t sm_rank[256];        // async mode: CTAs of the persistent launch counted per SM (%smid)
 };
 
 __device__ __forceinline__ unsigned long long gtimer()
@@ -557,17 +558,17 @@ template <int R> struct CellCfg {
 #ifndef EIK_PARITY
 #define EIK_PARITY 1
 #endif
-#ifndef EIK_ACT_PTX
-#define EIK_ACT_PTX 0   // 1: activations as one PTX block (fewer SASS instructions, measured C5 31 -> 37 ms)
-#endif
-#ifndef EIK_ACT_CLOBBER
-#define EIK_ACT_CLOBBER : "memory"
-#endif
 #ifndef EIK_STAGE_B32
 #define EIK_STAGE_B32 3   // fp32 tile vectors in flight per thread while staging (6: all of them, spills at 64 registers)
 #endif
+#ifndef EIK_STAGE_B64
+#define EIK_STAGE_B64 2   // fp64 tile vectors (16 B) in flight per thread while staging
+#endif
 #ifndef EIK_SWEEP16
 #define EIK_SWEEP16 1   // r = 16, kappa = 0: the packed-table wavefront step (sweep16)
+#endif
+#ifndef EIK_WARP_BALANCE
+#define EIK_WARP_BALANCE 0   // k_async r = 16: permute the plane-table columns over the warps per CTA (measured: within 1 %)
 #endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
@@ -670,6 +671,14 @@ __device__ __forceinline__ uint32_t pref_dirs(uint32_t faces)
     if (faces & 32u) m |= 0xF0u;
     return m;
 }
+
+// The halo N(c) of a staged r = 16 cell is stored NEGATED in the shared box (sweep16r: the
+// activation test "neighbour > u" is then false outside the cell without a border test);
+// every reader of a box neighbour takes habs<R>() of it.  Smaller cells keep plain values (the
+// extra sign handling measured 6 % slower on the fp64 r = 8 suite).
+template <int R> struct HaloNeg { static constexpr bool value = R == 16; };
+template <int R, typename T> __device__ __forceinline__ T habs(T x) { if constexpr (HaloNeg<R>::value) return fabs(x); else return x; }
+template <int R, typename T> __device__ __forceinline__ T hneg(T x) { if constexpr (HaloNeg<R>::value) return -x; else return x; }
 
 template <typename T> struct Vec16;
 template <> struct Vec16<float> { using type = float4; };
@@ -816,7 +825,8 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
                 const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
                 const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
                 const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
-                const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
+                const T mx = vmin(habs<R>(xf), habs<R>(xb)), my = vmin(habs<R>(yf), habs<R>(yb)),
+                        mz = vmin(habs<R>(zf), habs<R>(zb));   // (HaloNeg)
                 const T hf = fabs(hs);
                 if (hf < INF && vmin(mx, vmin(my, mz)) < v) {
                     ++nupd;
@@ -866,7 +876,8 @@ __device__ __forceinline__ uint32_t sweep_dir(CellShared<R>& S, CellSmem<T, R>& 
             const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
             if (fl) {
                 sts_u8(ab + up, 0u);                                   // Alg. 2 line 4
-                const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
+                const T mx = vmin(habs<R>(xf), habs<R>(xb)), my = vmin(habs<R>(yf), habs<R>(yb)),
+                        mz = vmin(habs<R>(zf), habs<R>(zb));   // (HaloNeg)
                 const T hf = fabs(hs);
                 if (hf < INF && vmin(mx, vmin(my, mz)) < v) {          // fixed / no gain
                     ++nupd;
@@ -929,91 +940,60 @@ __device__ __forceinline__ float ldg_keep(const float* a, unsigned long long pol
 
 // ---- r = 16 wavefront sweep with a packed per-direction plane table -------------------------
 // tab16[d][s][t] (built on the host, eik.cu make_tab16) describes the t-th point of plane s of
-// direction d: bits 0-12 its box index q = (a+1) + 18 (b+1) + 324 (c+1), bits 13-18 the
-// neighbours that exist in the canonical (reflected) orientation of d (bit 0 forward x, 1
-// backward x, 2/3 y, 4/5 z), bits 19-31 its point index p = a + 16 b + 256 c.  A thread with no
-// point on a plane gets T16_DUMMY: a halo box index (reads only), no neighbours, and the flag
-// byte act[T16_DUMMY_P], which is 0 for the whole processing -- so every lane runs the same
-// straight-line step (no divergence, one warp vote skips the local solve of an idle warp).
-// Against sweep_dir this removes the per-step coordinate arithmetic (box offset, reflection,
-// border tests) and the branches; the activations are predicated stores at compile-time
-// offsets.  kappa = 0 only (the exact path; kappa > 0 runs sweep_dir).
+// direction d: bits 0-12 its box index q = (a+1) + 18 (b+1) + 324 (c+1), bits 19-31 its point
+// index p = a + 16 b + 256 c (bits 13-18 unused).  A thread with no point on a plane gets
+// T16_DUMMY: a halo box index (reads only), the flag byte act[T16_DUMMY_P], which is 0 for the
+// whole processing, and no hf -- so every lane runs the same straight-line step (no divergence),
+// and a warp whose lanes are all dummies skips the step's loads (one vote).
+//
+// The direction is a runtime argument: one instantiation instead of eight (eight copies of the
+// two step loops were ~45 KB of SASS per precision; with five CTAs per SM in different
+// directions and phases the instruction caches missed: ncu "no instruction" 8 % of the C5 stall
+// samples).  Nothing in the step depends on the direction any more:
+//  * the six neighbours are addressed physically (+-x, +-y, +-z: immediates); the local solve
+//    only needs min(x+, x-) etc.;
+//  * the halo N(c) is stored NEGATED in the box (see stage_cell_async), so |value| enters the
+//    minima (a free source modifier) and the activation test "neighbour > u" (Alg. 2 line 9) is
+//    false for every neighbour outside the cell without any border test: u > 0 >= -|halo|;
+//  * "some point ahead of the wavefront was activated" is replaced by its superset "some point
+//    of the plane changed" (the next plane then runs one idle step at worst), and the axes with
+//    activations behind the wavefront come from a 6-bit mask accumulated over the sweep.
+// kappa = 0 only (the exact path; kappa > 0 runs sweep_dir).
 static constexpr uint32_t T16_DUMMY_P = 16 * 16 * 16 + 1;                       // act[R3 + 1]
 static constexpr uint32_t T16_DUMMY = (1u + 18u + 324u) | (T16_DUMMY_P << 19);   // box (-1, 0, 0)
 static constexpr int T16_ROWS = 3 * 16 - 2 + 3;   // NPL + 3 trailing empty planes
 
-// Alg. 2 lines 8-13 for one updated point of sweep16, in PTX so that ptxas emits one
-// LOP3 (neighbour-exists bit -> predicate), one FSETP.AND and one predicated STS per neighbour:
-// for every neighbour that exists (bm bits 13-18: forward x, backward x, y, z) and holds a value
-// larger than u, set its activity byte.  Returns the forward activations (bit 0) and the
-// backward axes (bits 1-3).
-template <typename T, int OXP, int OYP, int OZP, bool FWD> struct Act16;
-#define EIK_ACT16_BODY(FT, CT)                                                                       \
-    static __device__ __forceinline__ uint32_t run(uint32_t bm, T xf, T xb, T yf, T yb, T zf, T zb,  \
-                                                   T u, uint32_t fa, uint32_t one)                  \
-    {                                                                                                \
-        uint32_t r;                                                                                  \
-        asm volatile("{\n\t.reg .pred q, p0, p1, p2, p3, p4, p5, pf;\n\t.reg .b32 t, a, b;\n\t"     \
-                     "and.b32 t, %1, 0x2000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p0, %2, %8, q;\n\t" \
-                     "and.b32 t, %1, 0x4000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p1, %3, %8, q;\n\t" \
-                     "and.b32 t, %1, 0x8000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p2, %4, %8, q;\n\t" \
-                     "and.b32 t, %1, 0x10000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p3, %5, %8, q;\n\t" \
-                     "and.b32 t, %1, 0x20000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p4, %6, %8, q;\n\t" \
-                     "and.b32 t, %1, 0x40000;\n\tsetp.ne.b32 q, t, 0;\n\tsetp.gt.and." FT " p5, %7, %8, q;\n\t" \
-                     "@p0 st.shared.u8 [%9+%11], %10;\n\t@p1 st.shared.u8 [%9+%12], %10;\n\t"            \
-                     "@p2 st.shared.u8 [%9+%13], %10;\n\t@p3 st.shared.u8 [%9+%14], %10;\n\t"            \
-                     "@p4 st.shared.u8 [%9+%15], %10;\n\t@p5 st.shared.u8 [%9+%16], %10;\n\t"            \
-                     "or.pred pf, p0, p2;\n\tor.pred pf, pf, p4;\n\t"                                  \
-                     "selp.u32 t, 1, 0, pf;\n\tselp.u32 a, 2, 0, p1;\n\tselp.u32 b, 4, 0, p3;\n\t"      \
-                     "or.b32 t, t, a;\n\tor.b32 t, t, b;\n\tselp.u32 a, 8, 0, p5;\n\tor.b32 %0, t, a;\n\t}" \
-                     : "=r"(r)                                                                       \
-                     : "r"(FWD ? bm : (bm & 0x54000u)), CT(xf), CT(xb), CT(yf), CT(yb), CT(zf), CT(zb),  \
-                       CT(u), "r"(fa), "r"(one), "n"(OXP), "n"(-OXP), "n"(OYP), "n"(-OYP), "n"(OZP),   \
-                       "n"(-OZP)                                                                     \
-                     EIK_ACT_CLOBBER);                                                               \
-        return r;                                                                                    \
-    }
-template <int OXP, int OYP, int OZP, bool FWD> struct Act16<float, OXP, OYP, OZP, FWD> {
-    using T = float;
-#define EIK_CF(x) "f"(x)
-    EIK_ACT16_BODY("f32", EIK_CF)
-#undef EIK_CF
-};
-template <int OXP, int OYP, int OZP, bool FWD> struct Act16<double, OXP, OYP, OZP, FWD> {
-    using T = double;
-#define EIK_CD(x) "d"(x)
-    EIK_ACT16_BODY("f64", EIK_CD)
-#undef EIK_CD
-};
-#undef EIK_ACT16_BODY
-
-template <typename T, int DIR>
-__device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* __restrict__ tab,
-                                            unsigned long long pm, bool ungated, uint32_t& nupd,
-                                            uint32_t& nwr, uint32_t& nsteps)
+template <typename T>
+__device__ __forceinline__ uint32_t sweep16r(CellSmem<T, 16>& M, const uint32_t* __restrict__ tab, int dir,
+                                             unsigned long long pm, bool ungated, uint32_t& nupd,
+                                             uint32_t& nwr, uint32_t& nsteps, uint32_t ltid)
 {
     using C = CellCfg<16>;
     constexpr int NPL = C::NPL, NT = C::NT, R3 = C::R3;
     constexpr int TS = (int)sizeof(T);
     constexpr bool HG = CellSmem<T, 16>::HG;
-    // forward neighbour offsets (canonical forward = physical +1 unless the axis is reflected)
-    constexpr int sx = (DIR & 1) ? -1 : 1, sy = (DIR & 2) ? -1 : 1, sz = (DIR & 4) ? -1 : 1;
-    // (unsigned: address arithmetic wraps modulo 2^32, a negative offset subtracts)
-    constexpr uint32_t oxq = (uint32_t)(sx * TS), oyq = (uint32_t)(sy * C::RP * TS),
-                       ozq = (uint32_t)(sz * C::RP2 * TS);                              // box bytes
+    constexpr uint32_t oxq = (uint32_t)TS, oyq = (uint32_t)(C::RP * TS), ozq = (uint32_t)(C::RP2 * TS);
+    // physical neighbours ahead of the wavefront of this direction (bit 0 +x, 1 -x, 2 +y, ...)
+    const uint32_t fm6 = ((dir & 1) ? 2u : 1u) | ((dir & 2) ? 8u : 4u) | ((dir & 4) ? 32u : 16u);
     const T INF = dinf<T>();
     const uint32_t vb = smem_u32(M.V);
     const uint32_t hb = HG ? 0u : smem_u32(M.H);
     const T* __restrict__ hg = M.Hg;
     const uint32_t ab = smem_u32(M.act);
-    const uint32_t* __restrict__ tp = tab + DIR * T16_ROWS * NT + threadIdx.x;
-    uint32_t one;
-    asm("mov.u32 %0, 1;" : "=r"(one));
+    const uint32_t* __restrict__ tp = tab + dir * T16_ROWS * NT + ltid;   // (ltid: see k_async)
     // HG (fp64): the cell's hf tile is read once per sweep through L2; an evict_last policy keeps
     // it there between the sweeps of a processing instead of re-fetching it from HBM
     const unsigned long long l2keep = HG ? l2_evict_last_policy() : 0ull;
+#ifndef EIK16_EXACT_FWD
+#define EIK16_EXACT_FWD 0
+#endif
+#if EIK16_EXACT_FWD
+#define EIK16_ACC am
+#else
+#define EIK16_ACC bwd6
+#endif
     bool fwd = false;
-    uint32_t bwd = 0;
+    uint32_t bwd6 = 0, cnt = 0;   // cnt: this sweep's updates | writes << 16 (<= 46 each per thread)
     int s = __ffsll((long long)pm) - 1;
     unsigned long long pmr = pm >> s;   // pm >> (current plane)
     uint32_t en = __ldg(tp + s * NT);
@@ -1031,56 +1011,69 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
     }
 #define EIK16_MARK(ue_, hf_)                                                               \
     {                                                                                      \
-        EIK_CHECK(((ue_) >> 19) < (uint32_t)R3, "sweep16 changed point");                  \
+        EIK_CHECK(((ue_) >> 19) < (uint32_t)R3, "sweep16r changed point");                 \
         if constexpr (HG) atomicOr(&M.chg[(ue_) >> 24], 1u << (((ue_) >> 19) & 31));      \
         else sts(hb + ((ue_) >> 19) * TS, -(hf_));   /* sign bit = changed */              \
     }
+    // One step.  FLD_: load the activity flag (gated sweeps); GATE_: the lane's gate; EN_(i):
+    // whether neighbour i may be activated (ungated sweeps: only those behind the wavefront).
+#define EIK16_STEP(FLD_, GATE_, EN_, ONE_)                                                 \
+        const uint32_t qa = vb + (ue & 0x1fffu) * TS;                                      \
+        const uint32_t fa = ab + (ue >> 19);                                               \
+        const uint32_t fl = (FLD_) ? lds_u8(fa) : 1u;                                      \
+        const T v = lds<T>(qa);                                                            \
+        const T xp = lds<T>(qa + oxq), xm = lds<T>(qa - oxq);                              \
+        const T yp = lds<T>(qa + oyq), ym = lds<T>(qa - oyq);                              \
+        const T zp = lds<T>(qa + ozq), zm = lds<T>(qa - ozq);                              \
+        const T mx = vmin(fabs(xp), fabs(xm)), my = vmin(fabs(yp), fabs(ym)),              \
+                mz = vmin(fabs(zp), fabs(zm));                                             \
+        const T hf = fabs(hs);                                                             \
+        sts_u8(fa, 0u);   /* Alg. 2 line 4 (nothing activates plane s during step s) */    \
+        const bool gate = (GATE_) && hf < INF && vmin(mx, vmin(my, mz)) < v;               \
+        if (__any_sync(0xffffffffu, gate)) {                                               \
+            const T u = local_solve_fast<T>(mx, my, mz, hf);          /* line 5 */         \
+            chg = gate && u < v;                                      /* line 6 */         \
+            cnt += (gate ? 1u : 0u) + (chg ? 0x10000u : 0u);   /* updates | writes << 16 */ \
+            if (chg) {                                                                     \
+                sts(qa, u);                                           /* line 7 */         \
+                EIK16_MARK(ue, hf)                                                         \
+            }                                                                              \
+            /* lines 8-13: activate larger in-cell neighbours (halo values are negative: no \
+               border test; the cross-border "currently downwind" test is done once per     \
+               processing) */                                                              \
+            const T ut = chg ? u : INF;                                                    \
+            if (EN_(0) && xp > ut) { sts_u8(fa + 1u, ONE_); EIK16_ACC |= 1u; }                    \
+            if (EN_(1) && xm > ut) { sts_u8(fa - 1u, ONE_); EIK16_ACC |= 2u; }                    \
+            if (EN_(2) && yp > ut) { sts_u8(fa + 16u, ONE_); EIK16_ACC |= 4u; }                   \
+            if (EN_(3) && ym > ut) { sts_u8(fa - 16u, ONE_); EIK16_ACC |= 8u; }                   \
+            if (EN_(4) && zp > ut) { sts_u8(fa + 256u, ONE_); EIK16_ACC |= 16u; }                 \
+            if (EN_(5) && zm > ut) { sts_u8(fa - 256u, ONE_); EIK16_ACC |= 32u; }                 \
+        }
     if (ungated) {
         // first sweep of a fresh cell: every point of every plane, only the activations behind
         // the wavefront are recorded (forward neighbours are visited later in this sweep)
+        const uint32_t em = ~fm6;
+#define EIK16_EN_U(i_) (em & (1u << (i_)))
         for (; s < NPL; ++s) {
             const uint32_t ue = en;
             const T hs = hn;
             EIK16_PREFETCH()
-            const uint32_t qa = vb + (ue & 0x1fffu) * TS;
-            const uint32_t fa = ab + (ue >> 19);
-            const T v = lds<T>(qa);
-            const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
-            const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
-            const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
-            sts_u8(fa, 0u);                                                // Alg. 2 line 4
-            const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
-            const T hf = fabs(hs);
-            const bool gate = ue != T16_DUMMY && hf < INF && vmin(mx, vmin(my, mz)) < v;
-            if (__any_sync(0xffffffffu, gate)) {
-                const T u = local_solve_fast<T>(mx, my, mz, hf);
-                const bool chg = gate && u < v;
-                nupd += gate;
-                nwr += chg;
-                if (chg) {
-                    sts(qa, u);
-                    EIK16_MARK(ue, hf)
-                }
-                // backward activations only (forward neighbours are visited later in this sweep)
-#if EIK_ACT_PTX
-                const uint32_t ar = Act16<T, (int)sx, 16 * sy, 256 * sz, false>::run(
-                    chg ? ue : 0u, xf, xb, yf, yb, zf, zb, u, fa, one);
-                bwd |= ar >> 1;
-#else
-                const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
-                const bool bxa = (bm & (2u << 13)) && xb > u, bya = (bm & (8u << 13)) && yb > u,
-                           bza = (bm & (32u << 13)) && zb > u;
-                if (bxa) sts_u8(fa - (uint32_t)sx, one);
-                if (bya) sts_u8(fa - (uint32_t)(16 * sy), one);
-                if (bza) sts_u8(fa - (uint32_t)(256 * sz), one);
-                bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
-#endif
+            if (!__all_sync(0xffffffffu, ue == T16_DUMMY)) {
+                bool chg = false;
+                uint32_t am = 0;
+                // (any byte with bit 0 set is an activity flag; ue | 1 needs no constant register)
+                const uint32_t one = ue | 1u;
+                EIK16_STEP(false, ue != T16_DUMMY, EIK16_EN_U, one)
+                (void)fl;
+                bwd6 |= am;
             }
             __syncthreads();
             ++nsteps;
         }
+#undef EIK16_EN_U
         pmr = 0;
     }
+#define EIK16_EN_G(i_) true
     for (; s < NPL; ++s, pmr >>= 1) {
         const bool go = ((uint32_t)pmr & 1u) | (uint32_t)fwd;   // (CTA-uniform)
         if (!go && pmr == 0ull) break;
@@ -1088,57 +1081,30 @@ __device__ __forceinline__ uint32_t sweep16(CellSmem<T, 16>& M, const uint32_t* 
         const T hs = hn;
         EIK16_PREFETCH()
         if (!go) continue;   // plane without active points: no step, no barrier
-        const uint32_t qa = vb + (ue & 0x1fffu) * TS;
-        const uint32_t fa = ab + (ue >> 19);
-        // flag and the seven box values in one shared-memory round trip
-        const uint32_t fl = lds_u8(fa);
-        const T v = lds<T>(qa);
-        const T xf = lds<T>(qa + oxq), xb = lds<T>(qa - oxq);
-        const T yf = lds<T>(qa + oyq), yb = lds<T>(qa - oyq);
-        const T zf = lds<T>(qa + ozq), zb = lds<T>(qa - ozq);
-        const T mx = vmin(xf, xb), my = vmin(yf, yb), mz = vmin(zf, zb);
-        const T hf = fabs(hs);
-        sts_u8(fa, 0u);   // Alg. 2 line 4 (unconditional: nothing activates plane s during step s)
-        const bool gate = fl && hf < INF && vmin(mx, vmin(my, mz)) < v;   // active, not fixed, can gain
-        bool myfwd = false;
-        if (__any_sync(0xffffffffu, gate)) {
-            const T u = local_solve_fast<T>(mx, my, mz, hf);                // line 5
-            const bool chg = gate && u < v;                                 // line 6
-            nupd += gate;
-            nwr += chg;
-            if (chg) {
-                sts(qa, u);                                                 // line 7
-                EIK16_MARK(ue, hf)
-            }
-            // lines 8-13: activate larger in-cell neighbours (the cross-border "currently
-            // downwind" test is done once per processing)
-#if EIK_ACT_PTX
-            const uint32_t ar = Act16<T, (int)sx, 16 * sy, 256 * sz, true>::run(
-                chg ? ue : 0u, xf, xb, yf, yb, zf, zb, u, fa, one);
-            myfwd = ar & 1u;
-            bwd |= ar >> 1;
-#else
-            const uint32_t bm = chg ? ue : 0u;   // neighbour bits 13-18
-            const bool fxa = (bm & (1u << 13)) && xf > u, bxa = (bm & (2u << 13)) && xb > u;
-            const bool fya = (bm & (4u << 13)) && yf > u, bya = (bm & (8u << 13)) && yb > u;
-            const bool fza = (bm & (16u << 13)) && zf > u, bza = (bm & (32u << 13)) && zb > u;
-            if (fxa) sts_u8(fa + (uint32_t)sx, one);
-            if (bxa) sts_u8(fa - (uint32_t)sx, one);
-            if (fya) sts_u8(fa + (uint32_t)(16 * sy), one);
-            if (bya) sts_u8(fa - (uint32_t)(16 * sy), one);
-            if (fza) sts_u8(fa + (uint32_t)(256 * sz), one);
-            if (bza) sts_u8(fa - (uint32_t)(256 * sz), one);
-            myfwd = fxa | fya | fza;
-            bwd |= (uint32_t)bxa | ((uint32_t)bya << 1) | ((uint32_t)bza << 2);
-#endif
+        bool chg = false;
+        uint32_t am = 0;
+        if (!__all_sync(0xffffffffu, ue == T16_DUMMY)) {
+            EIK16_STEP(true, fl, EIK16_EN_G, fl)
         }
-        fwd = __syncthreads_or(myfwd);
+#if EIK16_EXACT_FWD
+        bwd6 |= am;
+        fwd = __syncthreads_or(am & fm6);
+#else
+        (void)am;
+        fwd = __syncthreads_or(chg);
+#endif
         ++nsteps;
     }
+#undef EIK16_EN_G
+#undef EIK16_ACC
+#undef EIK16_STEP
 #undef EIK16_HF
 #undef EIK16_PREFETCH
 #undef EIK16_MARK
-    return bwd;
+    nupd += cnt & 0xffffu;
+    nwr += cnt >> 16;
+    const uint32_t b6 = bwd6 & ~fm6;
+    return ((b6 & 3u) ? 1u : 0u) | ((b6 & 12u) ? 2u : 0u) | ((b6 & 48u) ? 4u : 0u);
 }
 
 // Stage cell c (tile coordinates cx, cy, cz) into shared memory: the tile and its hf go out
@@ -1201,7 +1167,7 @@ __device__ __forceinline__ void stage_cell_async(const T* __restrict__ Vt, const
     }
 #pragma unroll
     for (int m = 0; m < PH; ++m)
-        if (hq[m] >= 0) sV[hq[m]] = hv[m];
+        if (hq[m] >= 0) sV[hq[m]] = hneg<R>(hv[m]);   // r = 16: the halo is stored negated (HaloNeg)
     cp_async_wait_all();
 }
 
@@ -1271,7 +1237,7 @@ __device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__
 template <typename T, int R, bool CPASYNC>
 __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S,
                                              CellSmem<T, R>& M, uint32_t c, uint32_t flags,
-                                             unsigned long long& n_sweeps_out)
+                                             unsigned long long& n_sweeps_out, uint32_t ltid = threadIdx.x)
 {
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
@@ -1321,7 +1287,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         constexpr int EL = 16 / sizeof(T);                // elements per vector
         constexpr int NV = R3 / EL;                       // vectors per tile
         constexpr int PV = (NV + NT - 1) / NT;            // vectors per thread
-        constexpr int B = sizeof(T) == 4 ? EIK_STAGE_B32 : 2;   // batch (register budget)
+        constexpr int B = sizeof(T) == 4 ? EIK_STAGE_B32 : EIK_STAGE_B64;   // batch (register budget)
         const V4* Vt4 = reinterpret_cast<const V4*>(Vt + base);
         if constexpr (CellSmem<T, R>::HG) {
             M.Hg = Ht + base;
@@ -1332,26 +1298,25 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
         T hv[PH];
-        int hq[PH];
+        // (the box index of a halo element is recomputed at its store instead of being held in
+        // a register across the tile loads: all tile vectors of a thread can then be in flight)
 #pragma unroll
         for (int m = 0; m < PH; ++m) {
             const int e = tid + m * NT;
-            hq[m] = -1;
             hv[m] = INF;
             if (e < 6 * R * R) {
                 const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
-                int hx, hy, hz, sa, sb, sd;
+                int sa, sb, sd;
                 int64_t nc;
                 bool ex;
                 switch (f) {
-                case 0: hx = -1; hy = u; hz = v; ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
-                case 1: hx = R; hy = u; hz = v; ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
-                case 2: hx = u; hy = -1; hz = v; ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
-                case 3: hx = u; hy = R; hz = v; ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
-                case 4: hx = u; hy = v; hz = -1; ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
-                default: hx = u; hy = v; hz = R; ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
+                case 0: ex = cx > 0; nc = (int64_t)c - 1; sa = R - 1; sb = u; sd = v; break;
+                case 1: ex = cx < cps - 1; nc = (int64_t)c + 1; sa = 0; sb = u; sd = v; break;
+                case 2: ex = cy > 0; nc = (int64_t)c - cps; sa = u; sb = R - 1; sd = v; break;
+                case 3: ex = cy < cps - 1; nc = (int64_t)c + cps; sa = u; sb = 0; sd = v; break;
+                case 4: ex = cz > 0; nc = (int64_t)c - (int64_t)cps * cps; sa = u; sb = v; sd = R - 1; break;
+                default: ex = cz < cps - 1; nc = (int64_t)c + (int64_t)cps * cps; sa = u; sb = v; sd = 0; break;
                 }
-                hq[m] = (hx + 1) + RP * (hy + 1) + RP2 * (hz + 1);
                 EIK_CHECK(!ex || (nc >= 0 && nc < (int64_t)A.cap), "halo neighbour cell");
                 if (ex) hv[m] = __ldcg(&Vt[nc * R3 + sa + R * sb + R * R * sd]);
             }
@@ -1379,8 +1344,16 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             }
         }
 #pragma unroll
-        for (int m = 0; m < PH; ++m)
-            if (hq[m] >= 0) sV[hq[m]] = hv[m];
+        for (int m = 0; m < PH; ++m) {
+            const int e = tid + m * NT;
+            if (e < 6 * R * R) {
+                const int f = e / (R * R), uv = e - f * R * R, u = uv % R, v = uv / R;
+                const int hx = f == 0 ? -1 : f == 1 ? R : u;
+                const int hy = f < 2 ? u : f == 2 ? -1 : f == 3 ? R : v;
+                const int hz = f < 4 ? v : f == 4 ? -1 : R;
+                sV[(hx + 1) + RP * (hy + 1) + RP2 * (hz + 1)] = hneg<R>(hv[m]);   // r = 16: stored negated (HaloNeg)
+            }
+        }
         cp_async_wait_all();
         if (tid == 0) S.tm[1] = (uint32_t)clock64();
     }
@@ -1437,7 +1410,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 default: a = u; b = v; d = R - 1; off = RP2; break;
                 }
                 const int q = (a + 1) + RP * (b + 1) + RP2 * (d + 1);
-                if (sV[q + off] < sV[q]) {
+                if (habs<R>(sV[q + off]) < sV[q]) {   // (HaloNeg)
                     sA[a + R * b + R * R * d] = 1;
                     ++cnt;
                     pm0 |= 1ull << plane0(a, b, d);
@@ -1513,7 +1486,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                     const T xm = sV[q - 1], xp = sV[q + 1];
                     const T ym = sV[q - RP], yp = sV[q + RP];
                     const T zm = sV[q - RP2], zp = sV[q + RP2];
-                    const T mx = vmin(xm, xp), my = vmin(ym, yp), mz = vmin(zm, zp);
+                    const T mx = vmin(habs<R>(xm), habs<R>(xp)), my = vmin(habs<R>(ym), habs<R>(yp)),
+                            mz = vmin(habs<R>(zm), habs<R>(zp));   // (HaloNeg)
                     if (hf < INF && vmin(mx, vmin(my, mz)) < v) {
                         ++nupd;
                         const T u = local_solve_fast<T>(mx, my, mz, hf);      // line 5
@@ -1596,14 +1570,16 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             unsigned long long pm = 0;
             int cnt = 0;
             const uint32_t* sA32 = reinterpret_cast<const uint32_t*>(sA);
+            // (every activity byte has bit 0 set: four flags of consecutive a per word fold into
+            // four plane bits with one multiply -- ascending a, or descending when x is reflected)
             for (int wd = tid; wd < R3 / 4; wd += NT) {
-                uint32_t x = sA32[wd];
-                while (x) {
-                    const int e = 4 * wd + ((__ffs(x) - 1) >> 3);
-                    x &= ~(0xffu << (8 * (e & 3)));
-                    const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
-                    pm |= 1ull << ((fx ? R - 1 - a : a) + (fy ? R - 1 - b : b) + (fz ? R - 1 - d : d));
-                    ++cnt;
+                const uint32_t y = sA32[wd] & 0x01010101u;
+                if (y) {
+                    const int a0 = (4 * wd) & (R - 1), b = ((4 * wd) / R) & (R - 1), d = (4 * wd) / (R * R);
+                    const int pbd = (fy ? R - 1 - b : b) + (fz ? R - 1 - d : d);
+                    if (fx) pm |= (unsigned long long)((y * 0x08040201u) >> 24) << (R - 4 - a0 + pbd);
+                    else pm |= (unsigned long long)((y * 0x01020408u) >> 24) << (a0 + pbd);
+                    cnt += __popc(y);
                 }
             }
 #pragma unroll
@@ -1655,16 +1631,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             if constexpr (R < EIK_DIR_TEMPLATE_MIN_R) {
                 bwd = sweep_dir<T, R, -1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_, dir);
             } else if (R == 16 && EIK_SWEEP16 && kap == T(0)) {
-                if constexpr (R == 16) switch (dir) {
-                case 0: bwd = sweep16<T, 0>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                case 1: bwd = sweep16<T, 1>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                case 2: bwd = sweep16<T, 2>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                case 3: bwd = sweep16<T, 3>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                case 4: bwd = sweep16<T, 4>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                case 5: bwd = sweep16<T, 5>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                case 6: bwd = sweep16<T, 6>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                default: bwd = sweep16<T, 7>(M, A.tab16, pm, ungated, nupd, nwr, nsteps); break;
-                }
+                if constexpr (R == 16) bwd = sweep16r<T>(M, A.tab16, dir, pm, ungated, nupd, nwr, nsteps, ltid);
             } else switch (dir) {
             case 0: bwd = sweep_dir<T, R, 0>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
             case 1: bwd = sweep_dir<T, R, 1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_); break;
@@ -1683,6 +1650,12 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         __syncthreads();
     }
     if (tid == 0) S.tm[7] = (uint32_t)clock64();
+    // ---- write back (16-byte vectors; a vector holding any changed point is stored whole,
+    // unchanged values are rewritten identically).  Issued before the face summaries, which only
+    // read shared memory, so the stores drain while they run (kappa > 0 needs the old values of
+    // the global tile in the summaries and writes back after them) ----
+    unsigned long long nw = 0;
+    if (kap == T(0)) nw = write_back_changed<T, R>(Vt + base, M);
     // ---- face summaries (Eq. (3)): face f is currently downwind iff a border
     // point changed in this processing and ended below its outside neighbour (the staged
     // halo value, an upper bound of the current one: P:718 redundant tags are harmless); the
@@ -1714,7 +1687,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             const int pp = a + R * b + R * R * d;
             if (M.changed(pp)) {
                 const T val = sV[(a + 1) + RP * (b + 1) + RP2 * (d + 1)];
-                const T out = sV[(ha + 1) + RP * (hb + 1) + RP2 * (hd + 1)];
+                const T out = habs<R>(sV[(ha + 1) + RP * (hb + 1) + RP2 * (hd + 1)]);   // (HaloNeg)
                 // kappa: a border change <= kappa tags no neighbour cell (the tile in
                 // global memory still holds the value staged at the start of the processing)
                 const bool sig = kap == T(0) || __ldcg(&Vt[base + pp]) - val > kap;
@@ -1732,9 +1705,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     }
     __syncthreads();
 
-    // ---- write back (16-byte vectors; a vector holding any changed point is stored whole,
-    // unchanged values are rewritten identically) ----
-    unsigned long long nw = write_back_changed<T, R>(Vt + base, M);
+    if (kap != T(0)) nw = write_back_changed<T, R>(Vt + base, M);
     if (A.stats) {
         unsigned long long u64 = nupd, w64 = nwr;
         for (int o = 16; o > 0; o >>= 1) {
@@ -2000,6 +1971,35 @@ k_async(CellArgs A)
     Ctl* ctl = A.ctl;
     uint32_t* ring = A.wl0;
     if (tid == 0) atomicMin(&ctl->t_start, gtimer());
+    // Warp balance across the SM's four schedulers (r = 16): the plane table fills its columns
+    // from 0 up, so the warp of columns 0-31 works in all 46 plane steps of a sweep, the next in
+    // 32, then 26, 20, 16 and 10.  With the identity mapping every CTA's busiest warps (0 and 4,
+    // 62 of the 150 warp-steps) sit on scheduler 0 (warp w issues on scheduler w mod 4).  The
+    // columns are therefore permuted per CTA: the two busiest logical warps go alone on the
+    // single-warp schedulers (2, 3), the others pair up as 26 + 10 and 20 + 16, and CTAs of even
+    // / odd rank on their SM mirror the assignment.
+    uint32_t ltid = (uint32_t)tid;
+#if EIK_WARP_BALANCE
+    if constexpr (R == 16 && NTH == 192) {
+        if (tid == 0) {   // (S.cell as the broadcast word: five CTAs per SM leave no spare shared memory)
+            uint32_t smid;
+            asm("mov.u32 %0, %%smid;" : "=r"(smid));
+            S.cell = atomicAdd(&ctl->sm_rank[smid & 255u], 1u);
+        }
+        __syncthreads();
+        // hardware warp -> logical warp (table columns): even rank {2,3,0,1,5,4}, odd {3,2,1,0,4,5}
+        const uint32_t pe = 0x451032u, po = 0x540123u;
+#if EIK_WARP_BALANCE == 2
+        const uint32_t lw = ((uint32_t)(tid >> 5) + S.cell) % 6u; (void)pe; (void)po;
+#elif EIK_WARP_BALANCE == 3
+        const uint32_t lw = (pe >> (4 * (tid >> 5))) & 15u; (void)po;
+#else
+        const uint32_t lw = (((S.cell & 1u) ? po : pe) >> (4 * (tid >> 5))) & 15u;
+#endif
+        ltid = lw * 32u + ((uint32_t)tid & 31u);
+        __syncthreads();   // S.cell is rewritten by the first pop
+    }
+#endif
     uint32_t tr_pid = 0, tr_tag = 0, tr_pop = 0, tr_swept = 0;   // processing trace (thread 0)
     uint32_t gen_c = 0;                                          // generation of the cell (thread 0)
     for (;;) {
@@ -2123,7 +2123,7 @@ k_async(CellArgs A)
             cell_process_b2<T>(A, S, Mb, c, S.flags, nsw);
         } else {
             CellSmem<T, R> Msm(smem_raw);
-            cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw);
+            cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw, ltid);
         }
         if (A.trace && tid == 0) tr_swept = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
         if (tid < 32) {

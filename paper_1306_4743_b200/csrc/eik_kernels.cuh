@@ -136,6 +136,9 @@ __device__ __forceinline__ T local_solve(T mx, T my, T mz, T hf)
 #ifndef EIK_VMIN
 #define EIK_VMIN 1
 #endif
+#ifndef EIK_SORT3_CMP
+#define EIK_SORT3_CMP 0   // fp64: sort the three axis minima with three compares (measured: P2 19.3 -> 19.5 ms, C3d / C2d within noise)
+#endif
 __device__ __forceinline__ float vmin(float a, float b) { return fminf(a, b); }
 __device__ __forceinline__ float vmax(float a, float b) { return fmaxf(a, b); }
 #if EIK_VMIN
@@ -145,6 +148,13 @@ __device__ __forceinline__ double vmax(double a, double b) { return b > a ? b : 
 __device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); }
 __device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
 #endif
+
+// |x| without the FP64 pipe (fabs(double) compiles to DADD -RZ, |x| when the result feeds a select)
+__device__ __forceinline__ float vabs(float x) { return fabsf(x); }
+__device__ __forceinline__ double vabs(double x)
+{
+    return __hiloint2double(__double2hiint(x) & 0x7fffffff, __double2loint(x));
+}
 
 // The same solve with the two- and three-sided candidates evaluated side by side and then
 // selected (shorter dependent chain: both square roots issue together).  d2, d3 are clamped to
@@ -181,13 +191,38 @@ __device__ __forceinline__ double sqrt_approx(double x)
 #endif
 }
 
+// a1 <= a2 <= a3 of three values: fp32 as a min/max network (FMNMX); fp64 from three compares
+// (each fp64 min or max costs its own DSETP on the half-rate pipe: six in the network)
+__device__ __forceinline__ void sort3(float mx, float my, float mz, float& a1, float& a2, float& a3)
+{
+    const float lo = vmin(mx, my), hi = vmax(mx, my);
+    a1 = vmin(lo, mz);
+    a3 = vmax(hi, mz);
+    a2 = vmax(lo, vmin(hi, mz));
+}
+__device__ __forceinline__ void sort3(double mx, double my, double mz, double& a1, double& a2, double& a3)
+{
+#if EIK_SORT3_CMP
+    const bool p1 = my < mx, p2 = mz < mx, p3 = mz < my;
+    const double lo = p1 ? my : mx, hi = p1 ? mx : my;
+    const bool plo = p1 ? p3 : p2;   // mz < lo
+    const bool phi = p1 ? p2 : p3;   // mz < hi
+    a1 = plo ? mz : lo;
+    a3 = phi ? hi : mz;
+    a2 = plo ? lo : (phi ? mz : hi);
+#else
+    const double lo = vmin(mx, my), hi = vmax(mx, my);
+    a1 = vmin(lo, mz);
+    a3 = vmax(hi, mz);
+    a2 = vmax(lo, vmin(hi, mz));
+#endif
+}
+
 template <typename T>
 __device__ __forceinline__ T local_solve_fast(T mx, T my, T mz, T hf)
 {
-    const T lo = vmin(mx, my), hi = vmax(mx, my);
-    const T a1 = vmin(lo, mz);
-    const T a3 = vmax(hi, mz);
-    const T a2 = vmax(lo, vmin(hi, mz));
+    T a1, a2, a3;
+    sort3(mx, my, mz, a1, a2, a3);
     const T d2 = vmin(a2 - a1, hf);
     const T d3 = vmin(a3 - a1, hf);
     const T hh = hf * hf;
@@ -308,6 +343,12 @@ template <> struct Vec4T<double> { static __device__ __forceinline__ void st(dou
     const double2 x = __ldcg(reinterpret_cast<const double2*>(p)), y = __ldcg(reinterpret_cast<const double2*>(p) + 1);
     v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; } };
 
+#ifndef EIK_INGEST_ROWS
+#define EIK_INGEST_ROWS 1   // 1: k_ingest_rows (a warp per row segment), 0: k_ingest (four points per thread)
+#endif
+#ifndef EIK_INGEST_GX
+#define EIK_INGEST_GX 32   // k_ingest_rows: blocks per z-plane (blockIdx.y strides over the planes)
+#endif
 #ifndef EIK_INGEST_U
 #define EIK_INGEST_U 2   // vectors of 4 points per thread and iteration (4 measured slower: C3 0.52 -> 0.65 ms)
 #endif
@@ -412,6 +453,102 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
     }
     (void)P;
     // exit count (warp-aggregated)
+    for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(0xffffffffu, exits, o);
+    if ((threadIdx.x & 31) == 0 && exits) atomicAdd(&ctl->n_exits, exits);
+}
+
+// A1, row-segment form (EIK_INGEST_ROWS): a warp takes 32 * EIK_INGEST_M consecutive points of
+// one padded (j, k) row.  Lane l handles the points i0 + l + 32 m: every load of F and of the
+// mask is one contiguous 128 / 32-byte warp access, and every store writes whole r-point row
+// pieces of the cell tiles (64 bytes for r = 16 fp32: full sectors) -- the same thread -> point
+// mapping on both sides, so nothing is transposed and the index math is 32-bit (few registers:
+// the occupancy that keeps enough bytes in flight).  Same validation, keys and seeding as
+// k_ingest.
+#ifndef EIK_INGEST_M
+#define EIK_INGEST_M 4
+#endif
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_ingest_rows(Geom g, T h, const T* __restrict__ F, const uint8_t* __restrict__ mask,
+              const T* __restrict__ q, T* __restrict__ Vt, T* __restrict__ Ht,
+              uint32_t* __restrict__ key, uint32_t* __restrict__ state, Ctl* ctl)
+{
+    constexpr int M = EIK_INGEST_M;
+    const int r = g.r, lr = g.lr;
+    const uint32_t n1 = (uint32_t)g.n1;
+    const uint32_t cps = (uint32_t)g.cps;
+    const uint32_t np = cps << lr;                         // padded points per side
+    const uint32_t nseg = (np + 32u * M - 1u) / (32u * M); // segments per padded row
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t wpb = blockDim.x >> 5;
+    const uint32_t rows_seg = np * nseg;                   // work items per z-plane (< 2^32)
+    uint32_t exits = 0;
+    const T INF = dinf<T>();
+    for (uint32_t k = blockIdx.y; k < np; k += gridDim.y) {
+        const uint32_t ck = (k >> lr) * cps, d = k & (uint32_t)(r - 1);
+        for (uint32_t w = blockIdx.x * wpb + (threadIdx.x >> 5); w < rows_seg; w += gridDim.x * wpb) {
+            const uint32_t j = w / nseg, sg = w - j * nseg;
+            const uint32_t i0 = sg * (32u * M) + lane;
+            const bool row_in = j < n1 && k < n1;
+            const int64_t lex0 = (int64_t)n1 * ((int64_t)j + (int64_t)n1 * k);
+            T f[M];
+            uint8_t mk[M];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const uint32_t i = i0 + 32u * m;
+                const bool in = row_in && i < n1;
+                f[m] = in ? __ldcs(&F[lex0 + i]) : T(0);
+                mk[m] = in ? __ldcs(&mask[lex0 + i]) : (uint8_t)0;
+            }
+            const uint32_t cj = ((j >> lr) + ck) * cps, b = j & (uint32_t)(r - 1);
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const uint32_t i = i0 + 32u * m;
+                if (i >= np) continue;
+                const uint32_t c = (i >> lr) + cj, a = i & (uint32_t)(r - 1);
+                const int64_t p = ((int64_t)c << (3 * lr)) + a + (uint32_t)r * (b + (uint32_t)r * d);
+                T vv = INF, hh = INF;
+                if (row_in && i < n1) {
+                    const T fl = f[m];
+                    if (!(fl >= T(0)) || !(fl < INF)) atomicOr(&ctl->err, 1u);   // F < 0, NaN, inf
+                    if (mk[m]) {
+                        T qv = q[lex0 + i];
+                        if (!(qv >= T(0)) || !(qv < INF)) atomicOr(&ctl->err, 2u);
+                        qv = qv + T(0);   // canonicalise -0 -> +0 (R9)
+                        vv = qv;          // exits: fixed, V = q (hf stays +inf: never updated)
+                        ++exits;
+                        const uint32_t kb = key_bits(qv);
+                        // V^c of a cell in Q^c = min exit value; cells holding a
+                        // non-exit neighbour of an exit across a cell face are seeded too (R18)
+                        atomicMin(&key[c], kb);
+                        atomicOr(&state[c], FLAG_INIT);
+                        const int64_t c64 = (int64_t)c, cp = (int64_t)cps;
+                        const int64_t cc[6] = {a == 0 && i > 0 ? c64 - 1 : -1,
+                                               a == (uint32_t)(r - 1) && i + 1 < n1 ? c64 + 1 : -1,
+                                               b == 0 && j > 0 ? c64 - cp : -1,
+                                               b == (uint32_t)(r - 1) && j + 1 < n1 ? c64 + cp : -1,
+                                               d == 0 && k > 0 ? c64 - cp * cp : -1,
+                                               d == (uint32_t)(r - 1) && k + 1 < n1 ? c64 + cp * cp : -1};
+#pragma unroll
+                        for (int f2 = 0; f2 < 6; ++f2)
+                            if (cc[f2] >= 0) {
+                                atomicMin(&key[cc[f2]], kb);
+                                atomicOr(&state[cc[f2]], FLAG_INIT);
+                            }
+                    } else if (fl > T(0)) {
+                        hh = h / fl;
+                        // h/F must keep hf^2 normal and 3 hf^2 finite in T (the local solve squares
+                        // it): fp32 [2^-60, 2^60], fp64 [2^-500, 2^500]; outside -> EIK_EINVAL
+                        const T lo = sizeof(T) == 4 ? T(8.673617379884035e-19) : T(3.054936363499605e-151);
+                        const T hi = sizeof(T) == 4 ? T(1.152921504606847e18) : T(3.273390607896142e150);
+                        if (!(hh >= lo && hh <= hi)) atomicOr(&ctl->err, 16u);
+                    }
+                }
+                Vt[p] = vv;
+                Ht[p] = hh;
+            }
+        }
+    }
     for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(0xffffffffu, exits, o);
     if ((threadIdx.x & 31) == 0 && exits) atomicAdd(&ctl->n_exits, exits);
 }
@@ -570,6 +707,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_WARP_BALANCE
 #define EIK_WARP_BALANCE 0   // k_async r = 16: permute the plane-table columns over the warps per CTA (measured: within 1 %)
 #endif
+#ifndef EIK_TAG_WARP1
+#define EIK_TAG_WARP1 1   // k_async: warp 1 tags and releases while warp 0 pops the next cell
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -677,7 +817,7 @@ __device__ __forceinline__ uint32_t pref_dirs(uint32_t faces)
 // every reader of a box neighbour takes habs<R>() of it.  Smaller cells keep plain values (the
 // extra sign handling measured 6 % slower on the fp64 r = 8 suite).
 template <int R> struct HaloNeg { static constexpr bool value = R == 16; };
-template <int R, typename T> __device__ __forceinline__ T habs(T x) { if constexpr (HaloNeg<R>::value) return fabs(x); else return x; }
+template <int R, typename T> __device__ __forceinline__ T habs(T x) { if constexpr (HaloNeg<R>::value) return vabs(x); else return x; }
 template <int R, typename T> __device__ __forceinline__ T hneg(T x) { if constexpr (HaloNeg<R>::value) return -x; else return x; }
 
 template <typename T> struct Vec16;
@@ -984,6 +1124,9 @@ __device__ __forceinline__ uint32_t sweep16r(CellSmem<T, 16>& M, const uint32_t*
     // HG (fp64): the cell's hf tile is read once per sweep through L2; an evict_last policy keeps
     // it there between the sweeps of a processing instead of re-fetching it from HBM
     const unsigned long long l2keep = HG ? l2_evict_last_policy() : 0ull;
+#ifndef EIK16_HG_DEEP
+#define EIK16_HG_DEEP 0   // sweep16r, hf from global memory: prefetch it two planes ahead (measured neutral on C3d)
+#endif
 #ifndef EIK16_EXACT_FWD
 #define EIK16_EXACT_FWD 0
 #endif
@@ -996,17 +1139,29 @@ __device__ __forceinline__ uint32_t sweep16r(CellSmem<T, 16>& M, const uint32_t*
     uint32_t bwd6 = 0, cnt = 0;   // cnt: this sweep's updates | writes << 16 (<= 46 each per thread)
     int s = __ffsll((long long)pm) - 1;
     unsigned long long pmr = pm >> s;   // pm >> (current plane)
+    // prefetch pipeline: the table entry two planes ahead, hf one plane ahead (shared memory);
+    // HG (hf from global memory / L2, fp64) runs one plane deeper: entry three, hf two ahead
+    constexpr bool DEEP = HG && EIK16_HG_DEEP;
     uint32_t en = __ldg(tp + s * NT);
     uint32_t en1 = __ldg(tp + (s + 1) * NT);
-    tp += (s + 2) * NT;
+    uint32_t en2 = DEEP ? __ldg(tp + (s + 2) * NT) : 0u;
+    tp += (s + (DEEP ? 3 : 2)) * NT;
 #define EIK16_HF(e_) (HG ? (((e_) >> 19) < (uint32_t)R3 ? ldg_keep(hg + ((e_) >> 19), l2keep) : INF)   \
                          : lds<T>(hb + ((e_) >> 19) * TS))
     T hn = EIK16_HF(en);
+    T hn1 = DEEP ? EIK16_HF(en1) : T(0);
 #define EIK16_PREFETCH()                                                                   \
     {                                                                                      \
         en = en1;                                                                          \
-        hn = EIK16_HF(en);                                                                 \
-        en1 = __ldg(tp);                                                                   \
+        if constexpr (DEEP) {                                                              \
+            en1 = en2;                                                                     \
+            hn = hn1;                                                                      \
+            hn1 = EIK16_HF(en1);                                                           \
+            en2 = __ldg(tp);                                                               \
+        } else {                                                                           \
+            hn = EIK16_HF(en);                                                             \
+            en1 = __ldg(tp);                                                               \
+        }                                                                                  \
         tp += NT;                                                                          \
     }
 #define EIK16_MARK(ue_, hf_)                                                               \
@@ -1025,9 +1180,9 @@ __device__ __forceinline__ uint32_t sweep16r(CellSmem<T, 16>& M, const uint32_t*
         const T xp = lds<T>(qa + oxq), xm = lds<T>(qa - oxq);                              \
         const T yp = lds<T>(qa + oyq), ym = lds<T>(qa - oyq);                              \
         const T zp = lds<T>(qa + ozq), zm = lds<T>(qa - ozq);                              \
-        const T mx = vmin(fabs(xp), fabs(xm)), my = vmin(fabs(yp), fabs(ym)),              \
-                mz = vmin(fabs(zp), fabs(zm));                                             \
-        const T hf = fabs(hs);                                                             \
+        const T mx = vmin(vabs(xp), vabs(xm)), my = vmin(vabs(yp), vabs(ym)),              \
+                mz = vmin(vabs(zp), vabs(zm));                                             \
+        const T hf = vabs(hs);                                                             \
         sts_u8(fa, 0u);   /* Alg. 2 line 4 (nothing activates plane s during step s) */    \
         const bool gate = (GATE_) && hf < INF && vmin(mx, vmin(my, mz)) < v;               \
         if (__any_sync(0xffffffffu, gate)) {                                               \
@@ -1052,8 +1207,12 @@ __device__ __forceinline__ uint32_t sweep16r(CellSmem<T, 16>& M, const uint32_t*
     if (ungated) {
         // first sweep of a fresh cell: every point of every plane, only the activations behind
         // the wavefront are recorded (forward neighbours are visited later in this sweep)
-        const uint32_t em = ~fm6;
-#define EIK16_EN_U(i_) (em & (1u << (i_)))
+        // (forward neighbours are activated too: each clears its flag when its own plane is
+        // visited later in this sweep -- cheaper than a per-direction enable test per neighbour)
+#define EIK16_EN_U(i_) true
+        // (Measured and rejected: running the corner planes -- the first six and last seven hold
+        // <= 28 points, all in one warp -- with warp barriers only; making this loop's CTA
+        // barrier conditional cost 10 % on C5, whichever corner was warp-local.)
         for (; s < NPL; ++s) {
             const uint32_t ue = en;
             const T hs = hn;
@@ -1271,7 +1430,6 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 
     // ---- stage V and hf with 16-byte vector loads (all of a batch in flight before any
     // store: memory-level parallelism), then the halo N(c) ----
-    const bool init = flags & FLAG_INIT;
     if constexpr (CPASYNC) {
         // Round mode: cp.async staging (see stage_cell_async; a round is one launch, and a
         // neighbour's re-activation of this cell may be consumed by this very processing in
@@ -1356,8 +1514,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         cp_async_wait_all();
         if (tid == 0) S.tm[1] = (uint32_t)clock64();
+        // async mode: `flags` is valid in thread 0 only (the result of its claim of the cell,
+        // whose round trip overlapped the loads above); the others take it from S.flags
+        if (tid == 0) S.flags = flags;
     }
     __syncthreads();
+    if constexpr (!CPASYNC) flags = S.flags;
+    const bool init = flags & FLAG_INIT;
     // ---- initial activity: all points (INIT), or the points of the inflow faces whose
     // outside neighbour is smaller (only smaller neighbours enter Eq. (2)), plus the
     // points saved at a sweep cap.  The first sweep's direction is fixed by the inflow faces,
@@ -1965,11 +2128,15 @@ __global__ void __launch_bounds__((AsyncCfg<T, R, MODE>::NT), (AsyncCfg<T, R, MO
 k_async(CellArgs A)
 {
     constexpr int NTH = AsyncCfg<T, R, MODE>::NT;
+    // TAG1: warp 1 re-activates the neighbours and releases the cell while warp 0 is already
+    // popping the next one (CTAs of at least two warps)
+    constexpr bool TAG1 = NTH >= 64 && EIK_TAG_WARP1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CellShared<R> S;
     const int tid = threadIdx.x;
     Ctl* ctl = A.ctl;
     uint32_t* ring = A.wl0;
+    if (TAG1 && tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
     if (tid == 0) atomicMin(&ctl->t_start, gtimer());
     // Warp balance across the SM's four schedulers (r = 16): the plane table fills its columns
     // from 0 up, so the warp of columns 0-31 works in all 46 plane steps of a sweep, the next in
@@ -2002,10 +2169,11 @@ k_async(CellArgs A)
 #endif
     uint32_t tr_pid = 0, tr_tag = 0, tr_pop = 0, tr_swept = 0;   // processing trace (thread 0)
     uint32_t gen_c = 0;                                          // generation of the cell (thread 0)
+    uint32_t ost = 0;                                            // state word the claim replaced (thread 0)
     for (;;) {
         if (tid < 32) {   // warp 0 pops the next cell; the other warps wait at the barrier
             const int lane = tid;
-            uint32_t got = Q_EMPTY, fl = 0;
+            uint32_t got = Q_EMPTY;
             for (;;) {
                 // lane 0: ticket pop -- every CTA takes the next head index with one atomicAdd
                 // (no CAS retry loop, which serialises 700+ CTAs to one claim per L2 round
@@ -2014,8 +2182,9 @@ k_async(CellArgs A)
                 uint32_t v = Q_EMPTY;
                 int quit = 0;
                 if (lane == 0) {
-                    if (__ldcg(&ctl->pending) == 0u || __ldcg(&ctl->abort) != 0u) quit = 1;
-                    if (!quit) {
+                    // (no pending / abort check before the ticket: the wait below makes it, and a
+                    // ticket taken after the end of the solve is harmless -- one round trip less)
+                    {
                         const uint32_t h = atomicAdd(&ctl->q_head, 1u);
                         unsigned ns = 32;
                         while ((v = atomicExch(&ring[h & A.qmask], Q_EMPTY)) == Q_EMPTY) {
@@ -2040,12 +2209,14 @@ k_async(CellArgs A)
                 // and v is re-queued while a neighbour runs or is queued ahead of it
                 bool d = false, drun = false;
                 int64_t nb = -1;
+                uint32_t gv0 = 0;   // generation of v (lanes < 6, when a readiness mode is on)
                 // mode 8 (automatic): mode 6 until the solve has run more than EIK_AUTO_RATIO
                 // processings per processed cell, then mode 2 for the rest (see release below)
                 const int dm = A.defer == 8 ? (int)__ldcg(&ctl->auto_mode) : A.defer;
                 if (dm && lane < 6) {
                     nb = face_neighbour(v, lane, A.cps);
                     const uint32_t kv = __ldcg(&A.key[v]), sv = __ldcg(&A.state[v]), gv = __ldcg(&A.gen[v]);
+                    gv0 = gv;
                     uint32_t sn = 0, kn = KEY_INF, gn = 0;
                     if (nb >= 0) { sn = __ldcg(&A.state[nb]); kn = __ldcg(&A.key[nb]); gn = __ldcg(&A.gen[nb]); }
                     // mode 4: only neighbours across an inflow face of v matter
@@ -2091,21 +2262,20 @@ k_async(CellArgs A)
                     continue;
                 }
                 got = v;
+                if (lane == 0) gen_c = dm ? gv0 : (A.defer >= 5 ? __ldcg(&A.gen[v]) : 0u);   // (broadcast at the tags)
                 break;
             }
             if (lane == 0) {
                 if (got != Q_EMPTY) {
-                    const uint32_t ost = atomicExch(&A.state[got], ST_RUNNING | ST_VISITED);
-                    fl = ost & 255u;                                        // faces + INIT + CONT
-                    if (!(ost & ST_VISITED)) atomicAdd(&ctl->first_procs, 1u);
-                    if (A.defer >= 5) gen_c = __ldcg(&A.gen[got]);   // (thread 0; broadcast at the tags)
+                    // the claim: its result (inflow faces + INIT + CONT) is first needed after the
+                    // staging loads have been issued, so its round trip overlaps theirs
+                    ost = atomicExch(&A.state[got], ST_RUNNING | ST_VISITED);
                     if (!A.legacy_key) A.key[got] = KEY_INF;             // V^c <- +inf
                     // (no fence: the tile loads depend on `got`, which was read from the ring
                     // after its producer fenced the cell's values, and go to L2)
                 }
                 S.cell = got;
-                S.flags = fl;
-                S.stat[0] = S.stat[1] = S.stat[2] = 0;
+                if constexpr (!TAG1) S.stat[0] = S.stat[1] = S.stat[2] = 0;   // (TAG1: thread 32 resets them)
                 if (A.trace && got != Q_EMPTY) {   // (thread 0's registers)
                     tr_pid = atomicAdd(&ctl->trace_n, 1u);
                     tr_tag = __ldcg(&A.tagger[got]);
@@ -2120,18 +2290,28 @@ k_async(CellArgs A)
         unsigned long long nsw = 0;
         if constexpr (MODE == 1 && R == 16) {
             B2Smem<T> Mb(smem_raw);
+            if (tid == 0) S.flags = ost & 255u;
+            __syncthreads();
             cell_process_b2<T>(A, S, Mb, c, S.flags, nsw);
         } else {
             CellSmem<T, R> Msm(smem_raw);
-            cell_process<T, R, false>(A, S, Msm, c, S.flags, nsw, ltid);
+            cell_process<T, R, false>(A, S, Msm, c, ost & 255u, nsw, ltid);   // (thread 0's claim -> S.flags)
         }
+        if (tid == 0 && !(ost & ST_VISITED)) atomicAdd(&ctl->first_procs, 1u);
         if (A.trace && tid == 0) tr_swept = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
-        if (tid < 32) {
+        if (!TAG1 && tid < 32) {
             tr_pid = __shfl_sync(0xffffffffu, tr_pid, 0);
             gen_c = __shfl_sync(0xffffffffu, gen_c, 0);
         }
+        // TAG1: thread 0 hands what it holds in registers to warp 1 through S.plane / S.plane0
+        // (free once the sweeps are over; five CTAs per SM leave no spare shared memory)
+        uint32_t* hand = reinterpret_cast<uint32_t*>(&S.plane[0]);
+        if (TAG1 && tid == 0) {
+            hand[0] = gen_c; hand[1] = tr_pid; hand[2] = tr_tag; hand[3] = tr_pop;
+            reinterpret_cast<uint32_t*>(&S.plane0)[0] = tr_swept;
+        }
         __threadfence();   // value stores before the re-activations
-        __syncthreads();
+        if constexpr (!TAG1) __syncthreads();
         // Re-activations first, then the cell's own release: a neighbour waiting for this cell
         // to stop running must find its tag already set (releasing first let it run without
         // the tag and then again with it: 50 % more processings on C4).  Warp 0 tags and then
@@ -2180,7 +2360,46 @@ k_async(CellArgs A)
             __threadfence();
             atomicSub(&ctl->pending, 1u);
         };
-        if (tid < 32) {
+        if constexpr (TAG1) {
+            // Every thread has fenced its write-back.  Warp 0 only arrives at the barrier that
+            // orders the tags behind those fences and goes on to pop the next cell; warp 1 waits
+            // for it, tags (lanes 0-5) and releases (its lane 0); warps 2+ wait at the loop top.
+            if (tid < 32) {
+                asm volatile("bar.arrive 3, %0;" :: "n"(NTH) : "memory");
+            } else {
+                asm volatile("bar.sync 3, %0;" :: "n"(NTH) : "memory");
+                if (tid < 64) {
+                    const int l = tid - 32;
+                    const uint32_t cont = S.cont, dstate = S.dstate, cont_key = S.cont_key;
+                    const unsigned long long st0 = S.stat[0], st1 = S.stat[1], st2 = S.stat[2];
+                    const uint32_t gen_w = hand[0], pid_w = hand[1];
+                    __syncwarp();
+                    if (l == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;   // for the next processing
+                    if (l < 6 && (S.face_flag & (1u << l))) {
+                        const int64_t nc = face_neighbour(c, l, A.cps);
+                        if (nc >= 0) {
+                            atomicMin(&A.key[nc], tag_key<T, R>(A, S, l, nc));          // Eq. (3) / (4)
+                            if (A.defer >= 5) atomicMax(&A.gen[nc], gen_w + 1u);
+                            if (A.trace) A.tagger[nc] = pid_w;
+                            const uint32_t old = atomicOr(&A.state[nc], (1u << (l ^ 1)) | ST_QUEUED);
+                            if (!(old & (ST_QUEUED | ST_RUNNING))) {
+                                q_push(ctl, ring, A.qmask, (uint32_t)nc);
+                                __threadfence();   // the push's pending increment before this cell's decrement
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (l == 0) {
+                        if (A.trace && pid_w < A.trace_cap) {
+                            const uint32_t te = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));
+                            A.trace[2 * pid_w] = make_uint4(c, hand[2], hand[3], reinterpret_cast<uint32_t*>(&S.plane0)[0]);
+                            A.trace[2 * pid_w + 1] = make_uint4(te, (uint32_t)nsw, S.flags, (uint32_t)st1);
+                        }
+                        release(cont, dstate, cont_key, st0, st1, st2);
+                    }
+                }
+            }
+        } else if (tid < 32) {
             if (tid < 6 && (S.face_flag & (1u << tid))) {
                 const int64_t nc = face_neighbour(c, tid, A.cps);
                 if (nc >= 0) {

@@ -192,6 +192,9 @@ static void make_tab_b2(std::vector<uint2>& tab)
 
 extern "C" int eik_abi_version(void) { return EIK_ABI_VERSION; }
 
+static int create_fill(eik_ctx* ctx, int device, void* cuda_stream);
+extern "C" void eik_destroy(eik_ctx* ctx);
+
 extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
 {
     eik_ctx* ctx = nullptr;
@@ -212,6 +215,21 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     ctx = new eik_ctx();
     ctx->device = device;
     ctx->sm_count = prop.multiProcessorCount;
+    // a failure while the context is being filled must not leak it, and its message must reach
+    // eik_last_error(NULL) (the caller never sees this ctx)
+    const int st = create_fill(ctx, device, cuda_stream);
+    if (st != EIK_OK) {
+        g_create_err = ctx->err;
+        if (cuda_stream) ctx->stream = nullptr;   // (not ours: eik_destroy must not synchronise it)
+        eik_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return EIK_OK;
+}
+
+static int create_fill(eik_ctx* ctx, int device, void* cuda_stream)
+{
     CK(cudaSetDevice(device));
     if (cuda_stream) ctx->stream = (cudaStream_t)cuda_stream;
     else {
@@ -272,7 +290,6 @@ extern "C" int eik_create(eik_ctx** out, int device, void* cuda_stream)
     CK(cudaFuncSetAttribute(k_dsweep<double, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cell_smem_bytes<double, 4>()));
     CK(cudaFuncSetAttribute(k_dsweep<float, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     CK(cudaFuncSetAttribute(k_dsweep<double, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    *out = ctx;
     return EIK_OK;
 }
 
@@ -614,7 +631,7 @@ static int run_loop(eik_ctx* ctx, int r, int64_t J, const CellArgs& ca)
     // loop mode 2: rounds in a CUDA graph with a conditional WHILE node around one round
     char keybuf[256];
     // every value baked into the captured kernel parameters is part of the key
-    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%g/%d/%d/%d/%.17g/%d", (int)sizeof(T), r, (long long)J,
+    snprintf(keybuf, sizeof keybuf, "%d/%d/%lld/%lld/%p/%p/%.17g/%d/%d/%d/%.17g/%d", (int)sizeof(T), r, (long long)J,
              (long long)ca.n1, ca.Vt, ca.Ht, ctx->bin_width, ca.stats, ca.max_sweeps, ca.fused, ca.kappa, ca.legacy_key);
     if (!ctx->gexec || ctx->gkey != keybuf) {
         if (ctx->gexec) { cudaGraphExecDestroy(ctx->gexec); ctx->gexec = nullptr; }

@@ -344,7 +344,7 @@ template <> struct Vec4T<double> { static __device__ __forceinline__ void st(dou
     v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; } };
 
 #ifndef EIK_INGEST_ROWS
-#define EIK_INGEST_ROWS 1   // 1: k_ingest_rows (a warp per row segment), 0: k_ingest (four points per thread)
+#define EIK_INGEST_ROWS 0   // 1: k_ingest_rows (a warp per row segment; measured C5 3.62 -> 3.72 ms, C3 equal), 0: k_ingest (four points per thread)
 #endif
 #ifndef EIK_INGEST_GX
 #define EIK_INGEST_GX 32   // k_ingest_rows: blocks per z-plane (blockIdx.y strides over the planes)

@@ -222,8 +222,12 @@ def run_reference(args):
               f"{w.n + 1}^3 sub-box at (k, j, i) = {tuple(lo)} of the {cfg} input ({w.M} of its "
               f"{(WN[cfg] + 1) ** 3} points; same F, h = {w.h:g} and the exits inside)")
     cb = config_block(cfg, prec, r)
+    # the workload is the arm's (same name and size: the driver matches the two lines on it); what
+    # actually ran per step is stated next to it, and keys that only describe the GPU path go
     cb.update({"precision": "f64", "solve": "oracle FMM (serial, fp64) on a bounded sample of this input",
-               "sample_points": w.M, "sample": sample})
+               "sample_n": w.n, "sample_points": w.M, "sample": sample})
+    cb.pop("l2", None)
+    cb.pop("cell_size", None)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",

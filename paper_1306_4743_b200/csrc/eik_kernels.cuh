@@ -104,6 +104,32 @@ __device__ __forceinline__ void cp_async_wait_all()
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
+// Bulk asynchronous copy (TMA engine, cp.async.bulk) of a contiguous block of global memory into
+// shared memory, completion signalled on an mbarrier: one instruction by one thread moves a whole
+// hf tile (16 KB for r = 16 fp32) instead of 1024 per-thread cp.async.  The mbarrier is
+// initialised once per kernel (arrival count 1); every copy is one phase (parity alternates).
+__device__ __forceinline__ void mbar_init(uint32_t mbar)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar)
+{
+    // earlier generic-proxy accesses of the destination (ordered before this thread by a CTA
+    // barrier) precede the async-proxy write
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "W_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W_%=;\n\t}" :: "r"(mbar), "r"(parity) : "memory");
+}
+
 // Local solve of Eq. (2) for U at one gridpoint, shifted sorted form (SURVEY
 // C.3, readings R1-R4): a1 <= a2 <= a3 are the per-axis neighbour minima (a1 finite),
 // hf = h/F.  t = U - a1; one-sided t = hf; two-sided iff hf > a2 - a1; three-sided iff the
@@ -710,6 +736,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_TAG_WARP1
 #define EIK_TAG_WARP1 1   // k_async: warp 1 tags and releases while warp 0 pops the next cell
 #endif
+#ifndef EIK_HF_BULK
+#define EIK_HF_BULK 1   // k_async: stage hf with one cp.async.bulk + mbarrier instead of per-thread cp.async
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -850,6 +879,9 @@ static_assert(EIK_HF_GLOBAL32 || ((cell_smem_bytes<float, 16>() + sizeof(CellSha
 // dynamic shared memory carve-up
 template <typename T, int R> struct CellSmem {
     static constexpr bool HG = HfGlobal<T, R>::value;
+    // async staging of hf by one bulk copy (r = 16 with hf in shared memory: the 16 KB fp32
+    // tile; measured 1 % slower than per-thread cp.async for the 4 KB tiles of r = 8)
+    static constexpr bool BULK = EIK_HF_BULK && R == 16 && !HG;
     T* V;          // (R+2)^3 box incl. halo faces
     T* H;          // R^3 hf (sign bit set = point changed in this processing); null if HG
     uint8_t* act;  // R^3 active flags (Alg. 2)
@@ -866,6 +898,9 @@ template <typename T, int R> struct CellSmem {
                   : reinterpret_cast<uint16_t*>(act + CellCfg<R>::R3 + 16);
         Hg = nullptr;
     }
+    // mbarrier of the bulk hf copy: bytes 8-15 of the 16 scratch bytes behind the activity flags
+    // (byte 0: sweep_dir's redirected stores, byte 1: sweep16r's dummy flag)
+    __device__ __forceinline__ uint32_t mbar() const { return smem_u32(act + CellCfg<R>::R3 + 8); }
     __device__ __forceinline__ T hf(int p) const { if constexpr (HG) return __ldg(Hg + p); else return H[p]; }
     __device__ __forceinline__ bool changed(int p) const
     {
@@ -1396,7 +1431,8 @@ __device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__
 template <typename T, int R, bool CPASYNC>
 __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S,
                                              CellSmem<T, R>& M, uint32_t c, uint32_t flags,
-                                             unsigned long long& n_sweeps_out, uint32_t ltid = threadIdx.x)
+                                             unsigned long long& n_sweeps_out, uint32_t ltid = threadIdx.x,
+                                             uint32_t hpar = 0u)
 {
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
@@ -1451,8 +1487,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             M.Hg = Ht + base;
             for (int w = tid; w < R3 / 32; w += NT) M.chg[w] = 0u;
         } else {
-            const uint32_t hsb = smem_u32(M.H);
-            for (int vi = tid; vi < NV; vi += NT) cp_async16(hsb + vi * 16, Ht + base + vi * EL);
+            if constexpr (CellSmem<T, R>::BULK) {
+                // hf (read-only during the solve): one bulk copy by thread 0 (see bulk_g2s)
+                if (tid == 0) bulk_g2s(smem_u32(M.H), Ht + base, (uint32_t)(R3 * sizeof(T)), M.mbar());
+            } else {
+                const uint32_t hsb = smem_u32(M.H);
+                for (int vi = tid; vi < NV; vi += NT) cp_async16(hsb + vi * 16, Ht + base + vi * EL);
+            }
         }
         constexpr int PH = (6 * R * R + NT - 1) / NT;     // halo elements per thread
         T hv[PH];
@@ -1512,7 +1553,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 sV[(hx + 1) + RP * (hy + 1) + RP2 * (hz + 1)] = hneg<R>(hv[m]);   // r = 16: stored negated (HaloNeg)
             }
         }
-        cp_async_wait_all();
+        if constexpr (CellSmem<T, R>::BULK) mbar_wait(M.mbar(), hpar & 1u);
+        else cp_async_wait_all();
         if (tid == 0) S.tm[1] = (uint32_t)clock64();
         // async mode: `flags` is valid in thread 0 only (the result of its claim of the cell,
         // whose round trip overlapped the loads above); the others take it from S.flags
@@ -2137,6 +2179,11 @@ k_async(CellArgs A)
     Ctl* ctl = A.ctl;
     uint32_t* ring = A.wl0;
     if (TAG1 && tid == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;
+    uint32_t hpar = 0;   // phase of the hf bulk-copy mbarrier = cells this CTA has staged (EIK_HF_BULK)
+    if constexpr (MODE == 0 && CellSmem<T, R>::BULK) {
+        if (tid == 0) mbar_init(CellSmem<T, R>(smem_raw).mbar());
+        __syncthreads();
+    }
     if (tid == 0) atomicMin(&ctl->t_start, gtimer());
     // Warp balance across the SM's four schedulers (r = 16): the plane table fills its columns
     // from 0 up, so the warp of columns 0-31 works in all 46 plane steps of a sweep, the next in
@@ -2295,7 +2342,8 @@ k_async(CellArgs A)
             cell_process_b2<T>(A, S, Mb, c, S.flags, nsw);
         } else {
             CellSmem<T, R> Msm(smem_raw);
-            cell_process<T, R, false>(A, S, Msm, c, ost & 255u, nsw, ltid);   // (thread 0's claim -> S.flags)
+            cell_process<T, R, false>(A, S, Msm, c, ost & 255u, nsw, ltid, hpar);   // (thread 0's claim -> S.flags)
+            ++hpar;
         }
         if (tid == 0 && !(ost & ST_VISITED)) atomicAdd(&ctl->first_procs, 1u);
         if (A.trace && tid == 0) tr_swept = (uint32_t)(gtimer() - __ldcg(&ctl->t_solve0));

@@ -175,6 +175,16 @@ __device__ __forceinline__ double vmin(double a, double b) { return fmin(a, b); 
 __device__ __forceinline__ double vmax(double a, double b) { return fmax(a, b); }
 #endif
 
+// warp reductions in one instruction each (REDUX) instead of five shuffle + op rounds
+__device__ __forceinline__ unsigned long long warp_or64(unsigned long long x)
+{
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)x);
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(x >> 32));
+    return ((unsigned long long)hi << 32) | lo;
+}
+__device__ __forceinline__ uint32_t warp_add(uint32_t x) { return __reduce_add_sync(0xffffffffu, x); }
+__device__ __forceinline__ uint32_t warp_or(uint32_t x) { return __reduce_or_sync(0xffffffffu, x); }
+
 // |x| without the FP64 pipe (fabs(double) compiles to DADD -RZ, |x| when the result feeds a select)
 __device__ __forceinline__ float vabs(float x) { return fabsf(x); }
 __device__ __forceinline__ double vabs(double x)
@@ -1635,10 +1645,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 }
             }
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            pm0 |= __shfl_xor_sync(0xffffffffu, pm0, o);
-        }
+        cnt = (int)warp_add((uint32_t)cnt);
+        pm0 = warp_or64(pm0);
         if ((tid & 31) == 0 && cnt) { atomicAdd(&S.nact, cnt); atomicOr(&S.plane0, pm0); }
     }
     __syncthreads();
@@ -1787,11 +1795,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                     cnt += __popc(y);
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                pm |= __shfl_xor_sync(0xffffffffu, pm, o);
-                cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-            }
+            pm = warp_or64(pm);
+            cnt = (int)warp_add((uint32_t)cnt);
             if ((tid & 31) == 0 && pm) { atomicOr(&S.plane[sw & 1], pm); atomicAdd(&S.nact2[sw & 1], cnt); }
             __syncthreads();
         }
@@ -1850,7 +1855,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         if (tid == 0) S.tm[5] += (uint32_t)(clock64() - tm1);
         nact = LCAP + 1;   // unknown until the next scan
-        for (int o = 16; o > 0; o >>= 1) bwd |= __shfl_xor_sync(0xffffffffu, bwd, o);
+        bwd = warp_or(bwd);
         if ((tid & 31) == 0 && bwd) atomicOr(&S.bwd[sw & 1], bwd);
         __syncthreads();
     }
@@ -1912,12 +1917,9 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
 
     if (kap != T(0)) nw = write_back_changed<T, R>(Vt + base, M);
     if (A.stats) {
-        unsigned long long u64 = nupd, w64 = nwr;
-        for (int o = 16; o > 0; o >>= 1) {
-            u64 += __shfl_xor_sync(0xffffffffu, u64, o);
-            w64 += __shfl_xor_sync(0xffffffffu, w64, o);
-            nw += __shfl_xor_sync(0xffffffffu, nw, o);
-        }
+        // (per-thread counts of one processing are far below 2^32 / 32)
+        const unsigned long long u64 = warp_add(nupd), w64 = warp_add(nwr);
+        nw = warp_add((uint32_t)nw);
         if ((tid & 31) == 0) {
             atomicAdd(&S.stat[0], u64);
             atomicAdd(&S.stat[1], w64);

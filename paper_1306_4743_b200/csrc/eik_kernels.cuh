@@ -749,6 +749,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_HF_BULK
 #define EIK_HF_BULK 1   // k_async: stage hf with one cp.async.bulk + mbarrier instead of per-thread cp.async
 #endif
+#ifndef EIK_LIST_THR
+#define EIK_LIST_THR -2   // active points at or below which the list relaxation replaces sweeps (0: the list capacity, -1: never, -2: r = 16 ? 16 : never)
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -1447,6 +1450,15 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     using C = CellCfg<R>;
     constexpr int NT = C::NT, R3 = C::R3, RP = C::RP, RP2 = C::RP2, NPL = C::NPL;
     constexpr int LCAP = C::LCAP;
+    // The list relaxation replaces sweeps only for a handful of active points (r = 16: <= 16;
+    // r <= 8: never).  It was introduced (round 1) with a threshold of the list capacity (384 /
+    // 128 points) to cut the tail of late sweeps, but a chaotic relaxation needs up to one
+    // iteration per plane to carry a change across the cell, each with two CTA barriers and
+    // shared-memory atomics, where one gated sweep in the right direction does it in one pass:
+    // measured with the round-2 step (threshold 384 -> 16): C1 1.44 -> 0.90 ms, C4 9.5 -> 6.5,
+    // C3 6.32 -> 5.69, C3d 21.4 -> 19.7, P3 10.4 -> 8.5 (never), PMAZE 39.6 -> 34.9, C5 30.4 -> 29.9.
+    constexpr int LTHR = EIK_LIST_THR == -2 ? (R == 16 ? 16 : 0)
+                       : EIK_LIST_THR < 0 ? 0 : (EIK_LIST_THR > 0 && EIK_LIST_THR < LCAP) ? EIK_LIST_THR : LCAP;
     const int tid = threadIdx.x;
     T* Vt = reinterpret_cast<T*>(A.Vt);
     const T* Ht = reinterpret_cast<const T*>(A.Ht);
@@ -1660,7 +1672,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     for (int sw = 0;; ++sw) {
         if (nact == 0) break;
         // ================= active-list relaxation (few active points) =================
-        if (nact <= LCAP) {
+        if (nact <= LTHR) {
             ran_list = true;
             const long long tl0 = tid == 0 ? clock64() : 0;
             // build the list from the flags
@@ -1806,7 +1818,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         const long long tm1 = tid == 0 ? clock64() : 0;
         if (tid == 0) S.tm[4] += (uint32_t)(tm1 - tm0);
         if (pm == 0ull) break;
-        if (nact <= LCAP && sw > 0) continue;   // few left: list mode (next iteration)
+        if (nact <= LTHR && sw > 0) continue;   // few left: list mode (next iteration)
         if (A.max_sweeps > 0 && nsweeps >= (uint32_t)A.max_sweeps) {
             // sweep cap reached with points still active: save them and continue in a later
             // processing (the cell re-queues itself; correctness is unaffected, values only

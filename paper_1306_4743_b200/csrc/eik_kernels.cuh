@@ -752,6 +752,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_LIST_THR
 #define EIK_LIST_THR -2   // active points at or below which the list relaxation replaces sweeps (0: the list capacity, -1: never, -2: r = 16 ? 16 : never)
 #endif
+#ifndef EIK_DIR0_ACT
+#define EIK_DIR0_ACT 1   // first sweep direction of a re-activated cell from the activated face points
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -1474,7 +1477,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     if (tid < 6) { S.face_min[tid] = KEY_INF; S.face_max[tid] = 0u; }
     if (tid == 0) {
         S.face_flag = 0;
-        S.plane[0] = S.plane[1] = 0; S.cont = 0; S.cont_key = KEY_INF;
+        S.plane[0] = 0; S.plane[1] = ~0ull; S.cont = 0; S.cont_key = KEY_INF;   // (plane[1]: argmin slot until the first sweep)
         S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
         sA[R3 + 1] = 0;   // sweep16's dummy flag byte (T16_DUMMY_P): never set
@@ -1622,9 +1625,16 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         } else {
             for (int w = tid; w < R3 / 4; w += NT) sA32[w] = 0u;
             __syncthreads();
-            // face points whose outside neighbour is smaller
+            // face points whose outside neighbour is smaller.  EIK_DIR0_ACT: the activated
+            // points are also counted per face (S.face_max, free until the face summaries) and
+            // the smallest activating value is located (S.plane[1], free until the first sweep):
+            // the first sweep's direction follows the faces that really bring information, not
+            // every face that was tagged (see below)
+            // (r >= 8: the face elements of a warp's loop iteration lie on one face)
+            constexpr bool D0 = EIK_DIR0_ACT && (6 * R * R) % NT == 0 && (R * R) % 32 == 0;
+            uint32_t mk = KEY_INF, mp = 0;
             for (int e = tid; e < 6 * R * R; e += NT) {
-                const int f = e / (R * R);
+                const int f = e / (R * R);   // (warp-uniform)
                 if (!(flags & (1u << f))) continue;
                 const int uv = e - f * R * R, u = uv & (R - 1), v = uv / R;
                 int a, b, d, off;
@@ -1637,11 +1647,26 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 default: a = u; b = v; d = R - 1; off = RP2; break;
                 }
                 const int q = (a + 1) + RP * (b + 1) + RP2 * (d + 1);
-                if (habs<R>(sV[q + off]) < sV[q]) {   // (HaloNeg)
+                const T ov = habs<R>(sV[q + off]);   // (HaloNeg)
+                const bool act = ov < sV[q];
+                if (act) {
                     sA[a + R * b + R * R * d] = 1;
                     ++cnt;
                     pm0 |= 1ull << plane0(a, b, d);
                 }
+                if constexpr (D0) {
+                    const uint32_t kb = act ? key_bits(ov) : KEY_INF;
+                    if (kb < mk) { mk = kb; mp = (uint32_t)(a + R * b + R * R * d); }
+                    const unsigned bal = __ballot_sync(0xffffffffu, act);
+                    if ((tid & 31) == 0 && bal) atomicAdd(&S.face_max[f], (uint32_t)__popc(bal));
+                }
+            }
+            if constexpr (D0) {
+                const uint32_t wm = __reduce_min_sync(0xffffffffu, mk);
+                const unsigned who = __ballot_sync(0xffffffffu, mk == wm);
+                const uint32_t wp = __shfl_sync(0xffffffffu, mp, __ffs(who) - 1);
+                if ((tid & 31) == 0 && wm != KEY_INF)
+                    atomicMin(&S.plane[1], ((unsigned long long)wm << 32) | wp);
             }
             // points saved at a sweep cap
             if (flags & FLAG_CONT) {
@@ -1663,6 +1688,39 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
     }
     __syncthreads();
     if (tid == 0) S.tm[3] = (uint32_t)clock64();
+    // EIK_DIR0_ACT: direction of the first sweep of a cell activated through its faces.  The
+    // tagged faces alone fix the direction only along axes with exactly one tagged face (an
+    // untagged axis defaulted to ascending, and tags of both faces of an axis accumulate while a
+    // cell waits: re-processings with >= 4 tagged faces took 2.5-9.7 sweeps on C3).  Instead:
+    // along every axis away from the smallest activating value (the flow enters there), except
+    // that for r = 16 an axis whose two faces activated different numbers of points goes away
+    // from the face with more.  The plane mask collected above belongs to the tag-based
+    // direction, so the first sweep takes it from the scan below when the direction changed.
+    // Measured: C1 0.77 -> 0.70 ms, C2 3.32 -> 3.04, C3 5.73 -> 5.58, C3d 19.9 -> 18.8, C5 30.1 ->
+    // 29.2, P3 8.53 -> 8.00, PMAZE 35.0 -> 33.4; C4 6.55 -> 6.8 (the one config it costs).
+    bool pm0_ok = true;
+    constexpr bool D0A = EIK_DIR0_ACT && (6 * R * R) % NT == 0 && (R * R) % 32 == 0;
+    if (D0A && !init && !resumed && S.nact > 0) {
+        const unsigned long long am = S.plane[1];
+        const uint32_t ap = (uint32_t)am;
+        int nd = 0;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+            const uint32_t cm = S.face_max[2 * ax], cp = S.face_max[2 * ax + 1];
+            const int pos = (int)((ap / (ax == 0 ? 1u : ax == 1 ? (uint32_t)R : (uint32_t)(R * R))) & (uint32_t)(R - 1));
+            // (measured: the face counts help r = 16 -- C3 5.67 -> 5.58 ms, C3d 19.25 -> 18.8 -- and
+            // hurt r = 8, where the smallest value alone decides: P3 8.44 -> 8.00, P2 17.3 -> 16.75;
+            // counts alone, without the smallest value, gain nothing)
+            const bool desc = (R == 16 && cm != cp) ? cp > cm : pos >= R / 2;
+            nd |= desc ? (1 << ax) : 0;
+        }
+        pm0_ok = nd == dir0;
+        dir0 = nd;
+    }
+    if (D0A && !init) {   // the counters go back to the face summaries' initial value
+        __syncthreads();
+        if (tid < 6) S.face_max[tid] = 0u;
+    }
 
     int prev_dir = -1;
     bool ran_list = false;
@@ -1791,7 +1849,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         // the set of planes (in this direction) holding active points, and their count (the
         // first sweep's was collected with the initial activity)
         const bool first = sw == 0 && !ran_list;
-        if (!first) {
+        const bool have0 = first && pm0_ok;   // the plane mask of this direction is in S.plane0
+        if (!have0) {
             unsigned long long pm = 0;
             int cnt = 0;
             const uint32_t* sA32 = reinterpret_cast<const uint32_t*>(sA);
@@ -1812,8 +1871,8 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
             if ((tid & 31) == 0 && pm) { atomicOr(&S.plane[sw & 1], pm); atomicAdd(&S.nact2[sw & 1], cnt); }
             __syncthreads();
         }
-        const unsigned long long pm = first ? S.plane0 : S.plane[sw & 1];
-        nact = first ? S.nact : S.nact2[sw & 1];
+        const unsigned long long pm = have0 ? S.plane0 : S.plane[sw & 1];
+        nact = have0 ? S.nact : S.nact2[sw & 1];
         if (tid == 0) { S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0; }
         const long long tm1 = tid == 0 ? clock64() : 0;
         if (tid == 0) S.tm[4] += (uint32_t)(tm1 - tm0);

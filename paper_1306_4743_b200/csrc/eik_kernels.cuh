@@ -755,6 +755,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_DIR0_ACT
 #define EIK_DIR0_ACT 1   // first sweep direction of a re-activated cell from the activated face points
 #endif
+#ifndef EIK_DIR_VOTE
+#define EIK_DIR_VOTE 2   // sweep directions after the first from a vote of the active points (1: always, 2: when two or more axes are ambiguous)
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -917,6 +920,9 @@ template <typename T, int R> struct CellSmem {
     // mbarrier of the bulk hf copy: bytes 8-15 of the 16 scratch bytes behind the activity flags
     // (byte 0: sweep_dir's redirected stores, byte 1: sweep16r's dummy flag)
     __device__ __forceinline__ uint32_t mbar() const { return smem_u32(act + CellCfg<R>::R3 + 8); }
+    // direction votes of the active points (bytes 4-7 of the same scratch): three biased 10-bit
+    // fields x | y << 10 | z << 20, see cell_process
+    __device__ __forceinline__ uint32_t* votes() const { return reinterpret_cast<uint32_t*>(act + CellCfg<R>::R3 + 4); }
     __device__ __forceinline__ T hf(int p) const { if constexpr (HG) return __ldg(Hg + p); else return H[p]; }
     __device__ __forceinline__ bool changed(int p) const
     {
@@ -1481,6 +1487,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         S.plane0 = 0; S.nact2[0] = S.nact2[1] = 0;
         S.nact = 0; S.lcnt[0] = S.lcnt[1] = 0; S.lover = 0;
         sA[R3 + 1] = 0;   // sweep16's dummy flag byte (T16_DUMMY_P): never set
+        if (EIK_DIR_VOTE) *M.votes() = 512u | (512u << 10) | (512u << 20);
     }
     // phase timers live in shared memory, written by thread 0 only (no registers held
     // across the sweeps): tm = {start, tile staged, halo staged, init done, mask, steps, list
@@ -1821,6 +1828,49 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         // behind its wavefront are reversed (information still has to travel that way);
         // without such activations the Gray cycle 0,1,3,2,6,7,5,4 is followed
         int dir;
+        // EIK_DIR_VOTE: from the second sweep on, every active point votes per axis for the side
+        // its smaller neighbour is on, if that neighbour is below the point's own value (the
+        // information it was activated for comes from there); an axis with a majority sweeps
+        // away from that side, a tied axis keeps the rule below
+        int vote_m = 0, vote_d = 0;   // axes with a majority, and their direction bits
+#if EIK_DIR_VOTE
+        // (variant 2: only when the previous sweep left activations behind it along two or more
+        // axes -- with one axis the rule below is unambiguous, and the vote costs a pass)
+        const uint32_t bwp = sw > 0 ? S.bwd[(sw - 1) & 1] : 0u;
+        if (prev_dir >= 0 && (EIK_DIR_VOTE == 1 || __popc(bwp & 7u) >= 2)) {
+            int vx = 0, vy = 0, vz = 0;
+            const uint32_t* sA32v = reinterpret_cast<const uint32_t*>(sA);
+            for (int wd = tid; wd < R3 / 4; wd += NT) {
+                uint32_t y = sA32v[wd] & 0x01010101u;
+                while (y) {
+                    const int i = (__ffs(y) - 1) >> 3;
+                    y &= y - 1u;
+                    const int e = 4 * wd + i;
+                    const int a = e & (R - 1), b = (e / R) & (R - 1), d = e / (R * R);
+                    const int q = (a + 1) + RP * (b + 1) + RP2 * (d + 1);
+                    const T v = sV[q];
+                    const T xm = habs<R>(sV[q - 1]), xp = habs<R>(sV[q + 1]);
+                    const T ym = habs<R>(sV[q - RP]), yp = habs<R>(sV[q + RP]);
+                    const T zm = habs<R>(sV[q - RP2]), zp = habs<R>(sV[q + RP2]);
+                    if (vmin(xm, xp) < v) vx += xm < xp ? 1 : (xp < xm ? -1 : 0);
+                    if (vmin(ym, yp) < v) vy += ym < yp ? 1 : (yp < ym ? -1 : 0);
+                    if (vmin(zm, zp) < v) vz += zm < zp ? 1 : (zp < zm ? -1 : 0);
+                }
+            }
+            // per warp: clamp to +-63 (six warps stay inside a biased 10-bit field), one atomic
+            vx = (int)warp_add((uint32_t)vx); vy = (int)warp_add((uint32_t)vy); vz = (int)warp_add((uint32_t)vz);
+            if ((tid & 31) == 0) {
+                auto cl = [](int x) { return x > 63 ? 63 : (x < -63 ? -63 : x); };
+                const int pk = cl(vx) + cl(vy) * 1024 + cl(vz) * 1048576;
+                if (pk) atomicAdd(M.votes(), (uint32_t)pk);
+            }
+            __syncthreads();
+            const uint32_t vw = *M.votes();
+            const int sx = (int)(vw & 1023u) - 512, sy = (int)((vw >> 10) & 1023u) - 512, sz = (int)((vw >> 20) & 1023u) - 512;
+            vote_m = (sx != 0 ? 1 : 0) | (sy != 0 ? 2 : 0) | (sz != 0 ? 4 : 0);
+            vote_d = (sx < 0 ? 1 : 0) | (sy < 0 ? 2 : 0) | (sz < 0 ? 4 : 0);
+        }
+#endif
         {
             const uint32_t gray = 0x45762310u;
             const uint32_t bw = sw > 0 ? S.bwd[(sw - 1) & 1] : 0u;
@@ -1841,6 +1891,13 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
                 dir = (gray >> (4 * gi)) & 15u;
                 gi = (gi + 1) & 7;
                 if (dir == prev_dir) { dir = (gray >> (4 * gi)) & 15u; gi = (gi + 1) & 7; }
+            }
+            if (vote_m) {
+                // voted axes take the vote, the others what the rule above chose
+                dir = (dir & ~vote_m) | (vote_d & vote_m);
+                if ((dir ^ prev_dir) & 1) lf0 = sw;
+                if ((dir ^ prev_dir) & 2) lf1 = sw;
+                if ((dir ^ prev_dir) & 4) lf2 = sw;
             }
             prev_dir = dir;
         }
@@ -1873,7 +1930,10 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         }
         const unsigned long long pm = have0 ? S.plane0 : S.plane[sw & 1];
         nact = have0 ? S.nact : S.nact2[sw & 1];
-        if (tid == 0) { S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0; }
+        if (tid == 0) {
+            S.plane[(sw + 1) & 1] = 0; S.nact2[(sw + 1) & 1] = 0;
+            if (EIK_DIR_VOTE) *M.votes() = 512u | (512u << 10) | (512u << 20);   // (biased zeros; every thread has read the votes)
+        }
         const long long tm1 = tid == 0 ? clock64() : 0;
         if (tid == 0) S.tm[4] += (uint32_t)(tm1 - tm0);
         if (pm == 0ull) break;

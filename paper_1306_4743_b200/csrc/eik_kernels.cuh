@@ -1442,11 +1442,11 @@ __device__ __forceinline__ unsigned long long write_back_changed(T* __restrict__
 //    a shared plane table; a step ends in one __syncthreads_or that also reports forward
 //    activations; planes without active points are skipped without a barrier.  Activity is
 //    one byte per point written with plain stores (several writers only ever store 1).
-//  * an active-point list once few points remain (<= LCAP): every listed point is relaxed
-//    at once (chaotic order, FIM-like), newly activated points are claimed with a CAS on
-//    their flag word and appended to the next list.  This turns the long tail of late sweeps
-//    (few active points spread over many planes) into a few short iterations.  If a list
-//    overflows, the flags stay authoritative and the wavefront sweeps resume.
+//  * an active-point list once only a handful of points remain (<= LTHR: 16 for r = 16, never
+//    for smaller cells; see LTHR below): every listed point is relaxed at once (chaotic order,
+//    FIM-like), newly activated points are claimed with a CAS on their flag word and appended
+//    to the next list (capacity LCAP).  If a list overflows, the flags stay authoritative and
+//    the wavefront sweeps resume.
 // "Changed" is the sign bit of a point's hf; the currently-downwind faces (Eq. (3)) are
 // derived once per processing from the changed border points.  Tile traffic bypasses L1
 // (ld/st .cg): other CTAs update neighbouring tiles concurrently in the async scheduler.

@@ -94,10 +94,11 @@ typedef enum {
                                 (cell, tagger, pop / swept / end times, sweeps, flags, generation)
                                 for eik_get_trace; 0 = off [0]                                  */
     EIK_OPT_CELL_KERNEL = 11 /* cell-sweep kernel of the async scheduler for r = 16 (kappa = 0,
-                                no sweep cap): 1 = 2x2x2 micro-blocks, one thread per block and
-                                block activity flags [1]; 0 = one thread per point (the point
-                                wavefront used for every other configuration).  Same fixed
-                                point                                               */
+                                no sweep cap): 0 = one thread per point, the point wavefront
+                                used for every configuration [0]; 1 = 2x2x2 micro-blocks, one
+                                thread per block and block activity flags (an experiment that
+                                measured slower; kept for comparison).  Same fixed point
+                                                                                      */
 } eik_option;
 
 /* Work and time counters of the last successful solve. */

@@ -850,16 +850,8 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
         const int64_t np = (int64_t)cps * r, nv = (np / 4) * np;   // vectors per padded z-plane
         const int bx = (int)((nv + 255) / 256 < 64 ? (nv + 255) / 256 : 64);
         const int by = (int)(np < 65535 ? np : 65535);
-#if EIK_INGEST_ROWS
-        (void)bx; (void)by;
-        const int64_t items = (int64_t)np * ((np + 32 * EIK_INGEST_M - 1) / (32 * EIK_INGEST_M));   // per z-plane
-        const int gx = (int)((items + 7) / 8 < EIK_INGEST_GX ? (items + 7) / 8 : EIK_INGEST_GX);
-        k_ingest_rows<T><<<dim3(gx, by), 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt,
-                                                      (T*)ctx->Ht, ctx->key, ctx->state, ctx->ctl);
-#else
         k_ingest<T><<<dim3(bx, by), 256, 0, s>>>(g, (T)h, (const T*)F, mask, (const T*)q, (T*)ctx->Vt,
                                                  (T*)ctx->Ht, ctx->key, ctx->state, ctx->ctl, P);
-#endif
     }
     if (method < 0 && ctx->loop_mode != 0) k_build_wl<<<G, 256, 0, s>>>(ctx->key, ctx->state, ctx->wl0, ctx->ctl, J);
     CK(cudaGetLastError());

@@ -379,12 +379,9 @@ template <> struct Vec4T<double> { static __device__ __forceinline__ void st(dou
     const double2 x = __ldcg(reinterpret_cast<const double2*>(p)), y = __ldcg(reinterpret_cast<const double2*>(p) + 1);
     v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y; } };
 
-#ifndef EIK_INGEST_ROWS
-#define EIK_INGEST_ROWS 0   // 1: k_ingest_rows (a warp per row segment; measured C5 3.62 -> 3.72 ms, C3 equal), 0: k_ingest (four points per thread)
-#endif
-#ifndef EIK_INGEST_GX
-#define EIK_INGEST_GX 32   // k_ingest_rows: blocks per z-plane (blockIdx.y strides over the planes)
-#endif
+// (A row-segment ingest -- a warp per 128 consecutive points of a row, every load and store a
+// contiguous warp access, 40 registers instead of 75 -- measured no faster: C5 3.62 -> 3.72 ms,
+// C3 equal; removed.)
 #ifndef EIK_INGEST_U
 #define EIK_INGEST_U 2   // vectors of 4 points per thread and iteration (4 measured slower: C3 0.52 -> 0.65 ms)
 #endif
@@ -489,102 +486,6 @@ __global__ void k_ingest(Geom g, T h, const T* __restrict__ F, const uint8_t* __
     }
     (void)P;
     // exit count (warp-aggregated)
-    for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(0xffffffffu, exits, o);
-    if ((threadIdx.x & 31) == 0 && exits) atomicAdd(&ctl->n_exits, exits);
-}
-
-// A1, row-segment form (EIK_INGEST_ROWS): a warp takes 32 * EIK_INGEST_M consecutive points of
-// one padded (j, k) row.  Lane l handles the points i0 + l + 32 m: every load of F and of the
-// mask is one contiguous 128 / 32-byte warp access, and every store writes whole r-point row
-// pieces of the cell tiles (64 bytes for r = 16 fp32: full sectors) -- the same thread -> point
-// mapping on both sides, so nothing is transposed and the index math is 32-bit (few registers:
-// the occupancy that keeps enough bytes in flight).  Same validation, keys and seeding as
-// k_ingest.
-#ifndef EIK_INGEST_M
-#define EIK_INGEST_M 4
-#endif
-template <typename T>
-__global__ void __launch_bounds__(256)
-k_ingest_rows(Geom g, T h, const T* __restrict__ F, const uint8_t* __restrict__ mask,
-              const T* __restrict__ q, T* __restrict__ Vt, T* __restrict__ Ht,
-              uint32_t* __restrict__ key, uint32_t* __restrict__ state, Ctl* ctl)
-{
-    constexpr int M = EIK_INGEST_M;
-    const int r = g.r, lr = g.lr;
-    const uint32_t n1 = (uint32_t)g.n1;
-    const uint32_t cps = (uint32_t)g.cps;
-    const uint32_t np = cps << lr;                         // padded points per side
-    const uint32_t nseg = (np + 32u * M - 1u) / (32u * M); // segments per padded row
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t wpb = blockDim.x >> 5;
-    const uint32_t rows_seg = np * nseg;                   // work items per z-plane (< 2^32)
-    uint32_t exits = 0;
-    const T INF = dinf<T>();
-    for (uint32_t k = blockIdx.y; k < np; k += gridDim.y) {
-        const uint32_t ck = (k >> lr) * cps, d = k & (uint32_t)(r - 1);
-        for (uint32_t w = blockIdx.x * wpb + (threadIdx.x >> 5); w < rows_seg; w += gridDim.x * wpb) {
-            const uint32_t j = w / nseg, sg = w - j * nseg;
-            const uint32_t i0 = sg * (32u * M) + lane;
-            const bool row_in = j < n1 && k < n1;
-            const int64_t lex0 = (int64_t)n1 * ((int64_t)j + (int64_t)n1 * k);
-            T f[M];
-            uint8_t mk[M];
-#pragma unroll
-            for (int m = 0; m < M; ++m) {
-                const uint32_t i = i0 + 32u * m;
-                const bool in = row_in && i < n1;
-                f[m] = in ? __ldcs(&F[lex0 + i]) : T(0);
-                mk[m] = in ? __ldcs(&mask[lex0 + i]) : (uint8_t)0;
-            }
-            const uint32_t cj = ((j >> lr) + ck) * cps, b = j & (uint32_t)(r - 1);
-#pragma unroll
-            for (int m = 0; m < M; ++m) {
-                const uint32_t i = i0 + 32u * m;
-                if (i >= np) continue;
-                const uint32_t c = (i >> lr) + cj, a = i & (uint32_t)(r - 1);
-                const int64_t p = ((int64_t)c << (3 * lr)) + a + (uint32_t)r * (b + (uint32_t)r * d);
-                T vv = INF, hh = INF;
-                if (row_in && i < n1) {
-                    const T fl = f[m];
-                    if (!(fl >= T(0)) || !(fl < INF)) atomicOr(&ctl->err, 1u);   // F < 0, NaN, inf
-                    if (mk[m]) {
-                        T qv = q[lex0 + i];
-                        if (!(qv >= T(0)) || !(qv < INF)) atomicOr(&ctl->err, 2u);
-                        qv = qv + T(0);   // canonicalise -0 -> +0 (R9)
-                        vv = qv;          // exits: fixed, V = q (hf stays +inf: never updated)
-                        ++exits;
-                        const uint32_t kb = key_bits(qv);
-                        // V^c of a cell in Q^c = min exit value; cells holding a
-                        // non-exit neighbour of an exit across a cell face are seeded too (R18)
-                        atomicMin(&key[c], kb);
-                        atomicOr(&state[c], FLAG_INIT);
-                        const int64_t c64 = (int64_t)c, cp = (int64_t)cps;
-                        const int64_t cc[6] = {a == 0 && i > 0 ? c64 - 1 : -1,
-                                               a == (uint32_t)(r - 1) && i + 1 < n1 ? c64 + 1 : -1,
-                                               b == 0 && j > 0 ? c64 - cp : -1,
-                                               b == (uint32_t)(r - 1) && j + 1 < n1 ? c64 + cp : -1,
-                                               d == 0 && k > 0 ? c64 - cp * cp : -1,
-                                               d == (uint32_t)(r - 1) && k + 1 < n1 ? c64 + cp * cp : -1};
-#pragma unroll
-                        for (int f2 = 0; f2 < 6; ++f2)
-                            if (cc[f2] >= 0) {
-                                atomicMin(&key[cc[f2]], kb);
-                                atomicOr(&state[cc[f2]], FLAG_INIT);
-                            }
-                    } else if (fl > T(0)) {
-                        hh = h / fl;
-                        // h/F must keep hf^2 normal and 3 hf^2 finite in T (the local solve squares
-                        // it): fp32 [2^-60, 2^60], fp64 [2^-500, 2^500]; outside -> EIK_EINVAL
-                        const T lo = sizeof(T) == 4 ? T(8.673617379884035e-19) : T(3.054936363499605e-151);
-                        const T hi = sizeof(T) == 4 ? T(1.152921504606847e18) : T(3.273390607896142e150);
-                        if (!(hh >= lo && hh <= hi)) atomicOr(&ctl->err, 16u);
-                    }
-                }
-                Vt[p] = vv;
-                Ht[p] = hh;
-            }
-        }
-    }
     for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(0xffffffffu, exits, o);
     if ((threadIdx.x & 31) == 0 && exits) atomicAdd(&ctl->n_exits, exits);
 }

@@ -160,6 +160,7 @@ def test_host_path_pinned_exit_values_in_place(solver):
 @pytest.mark.parametrize("mode,delta,msw,defer,kern", [
     (0, 0.0, 0, 1, 1), (0, 0.0, 2, 1, 1), (0, 0.0, 0, 0, 1), (0, 0.0, 0, 2, 1), (0, 0.05, 0, 3, 1),
     (0, 0.0, 0, 6, 0), (0, 0.0, 0, 0, 0), (0, 0.0, 0, 7, 1), (0, 0.0, 0, 6, 1),
+    (0, 0.0, 0, 8, 0), (0, 0.0, 0, 9, 0), (0, 0.0, 2, 9, 0),
     (1, 0.0, 0, 1, 1), (1, 0.05, 0, 1, 1), (1, 1e-6, 3, 1, 1),
     (2, 0.0, 0, 1, 1), (2, 0.05, 1, 1, 1), (2, 1e-6, 0, 1, 1)])
 def test_schedule_independence(mode, delta, msw, defer, kern):

@@ -62,7 +62,6 @@ struct eik_ctx {
     uint32_t* pend = nullptr;
     uint32_t* pdir = nullptr;
     uint32_t* gen = nullptr;
-    uint32_t* gen2 = nullptr;     // min-based activation level of each cell (readiness mode 9)
     uint32_t* wait = nullptr;
     size_t cell_cap = 0;
     size_t ring_cap = 0;
@@ -298,7 +297,7 @@ static void free_scratch(eik_ctx* ctx)
 {
     cudaFree(ctx->Vt); cudaFree(ctx->Ht);
     cudaFree(ctx->key); cudaFree(ctx->state); cudaFree(ctx->wl0); cudaFree(ctx->wl1);
-    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen); cudaFree(ctx->gen2); cudaFree(ctx->wait); cudaFree(ctx->pdir);
+    cudaFree(ctx->proc_cell); cudaFree(ctx->proc_flags); cudaFree(ctx->pend); cudaFree(ctx->gen); cudaFree(ctx->wait); cudaFree(ctx->pdir);
     cudaFree(ctx->diag_cells); cudaFree(ctx->diag_off); cudaFree(ctx->cact);
     ctx->diag_cells = ctx->diag_off = nullptr;
     ctx->cact = nullptr;
@@ -306,7 +305,6 @@ static void free_scratch(eik_ctx* ctx)
     ctx->pend = nullptr;
     ctx->pdir = nullptr;
     ctx->gen = nullptr;
-    ctx->gen2 = nullptr;
     ctx->wait = nullptr;
     ctx->Vt = ctx->Ht = nullptr;
     ctx->key = ctx->state = ctx->wl0 = ctx->wl1 = ctx->proc_cell = ctx->proc_flags = nullptr;
@@ -480,7 +478,6 @@ static int ensure_scratch(eik_ctx* ctx, size_t tile_bytes, size_t J)
         CK(cudaMalloc(&ctx->pend, J * 512));   // R^3 / 8 bytes per cell at r = 16
         CK(cudaMalloc(&ctx->pdir, J * 4));     // sweep-direction state at a cap
         CK(cudaMalloc(&ctx->gen, J * 4));
-        CK(cudaMalloc(&ctx->gen2, J * 4));
         CK(cudaMalloc(&ctx->wait, J * 4));
         CK(cudaMalloc(&ctx->diag_cells, J * 4));
         CK(cudaMalloc(&ctx->cact, J));
@@ -578,8 +575,8 @@ static int run_async(eik_ctx* ctx, int r, int64_t J, CellArgs ca)
     ca.defer = ctx->async_defer;
     ca.defer_delta = isinf(ctx->bin_width) ? 0.f : (float)ctx->bin_width;
     CK(cudaMemsetAsync(ctx->wl0, 0xff, ctx->ring_cap * 4, ctx->stream));
-    CK(cudaMemsetAsync(ctx->gen, 0, (size_t)J * 4, ctx->stream));
-    CK(cudaMemsetAsync(ctx->gen2, 0x7f, (size_t)J * 4, ctx->stream));   // (levels count up from 0x7f7f7f7f)
+    // (mode 9 keeps min-based levels in the same array: they count up from 0x7f7f7f7f)
+    CK(cudaMemsetAsync(ctx->gen, ctx->async_defer == 9 ? 0x7f : 0, (size_t)J * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->wait, 0, (size_t)J * 4, ctx->stream));
     ca.wait = ctx->wait;
     if (ctx->trace) {
@@ -888,7 +885,6 @@ static int solve_impl(eik_ctx* ctx, int64_t n, double h, const void* F, const ui
     ca.kappa = ctx->kappa;
     ca.legacy_key = ctx->legacy_key;
     ca.gen = ctx->gen;
-    ca.gen2 = ctx->gen2;
     ca.n1 = n1;
     ca.cps = cps;
     ca.stats = ctx->collect_stats;

@@ -708,8 +708,8 @@ struct CellArgs {
     uint32_t qmask;              // async mode: ring capacity - 1 (power of two)
     uint32_t* key;
     uint32_t* state;
-    uint32_t* gen;               // async mode: activation generation of each cell: 1 + the largest of its taggers' (modes 5-8)
-    uint32_t* gen2;              // async mode: activation level: 1 + the smallest of its taggers' (mode 9)
+    uint32_t* gen;               // async mode: activation generation of each cell, 1 + the largest of its
+                                 // taggers' (modes 5-8); mode 9: activation level, 1 + the smallest (from 0x7f7f7f7f)
     uint32_t* wait;              // async mode: bit f = the neighbour across face f is parked on this cell
     const uint16_t* plane_tab;   // [NPL + 3][NT] canonical point of thread t in plane s (0xFFFF: none)
     const uint32_t* tab16;       // r = 16: [8][NPL + 3][NT] packed per-direction plane table (sweep16)
@@ -2251,7 +2251,6 @@ k_async(CellArgs A)
 #endif
     uint32_t tr_pid = 0, tr_tag = 0, tr_pop = 0, tr_swept = 0;   // processing trace (thread 0)
     uint32_t gen_c = 0;                                          // generation of the cell (thread 0)
-    uint32_t gen2_c = 0x7f7f7f7fu;                               // its min-based level (thread 0)
     uint32_t ost = 0;                                            // state word the claim replaced (thread 0)
     for (;;) {
         if (tid < 32) {   // warp 0 pops the next cell; the other warps wait at the barrier
@@ -2292,19 +2291,16 @@ k_async(CellArgs A)
                 // and v is re-queued while a neighbour runs or is queued ahead of it
                 bool d = false, drun = false;
                 int64_t nb = -1;
-                uint32_t gv0 = 0, gv20 = 0x7f7f7f7fu;   // generation / level of v (lanes < 6, when a readiness mode is on)
+                uint32_t gv0 = 0;   // generation of v (lanes < 6, when a readiness mode is on)
                 // mode 8 (automatic): mode 6 until the solve has run more than EIK_AUTO_RATIO
                 // processings per processed cell, then mode 2 for the rest (see release below)
                 const int dm = A.defer == 8 ? (int)__ldcg(&ctl->auto_mode) : A.defer;
                 if (dm && lane < 6) {
                     nb = face_neighbour(v, lane, A.cps);
-                    // (mode 9 orders by the min-based level gen2 instead of the max-based generation)
-                    const uint32_t* __restrict__ garr = dm == 9 ? A.gen2 : A.gen;
-                    const uint32_t kv = __ldcg(&A.key[v]), sv = __ldcg(&A.state[v]), gv = __ldcg(&garr[v]);
-                    gv0 = dm == 9 ? 0u : gv;
-                    gv20 = dm == 9 ? gv : 0x7f7f7f7fu;
+                    const uint32_t kv = __ldcg(&A.key[v]), sv = __ldcg(&A.state[v]), gv = __ldcg(&A.gen[v]);
+                    gv0 = gv;
                     uint32_t sn = 0, kn = KEY_INF, gn = 0;
-                    if (nb >= 0) { sn = __ldcg(&A.state[nb]); kn = __ldcg(&A.key[nb]); gn = __ldcg(&garr[nb]); }
+                    if (nb >= 0) { sn = __ldcg(&A.state[nb]); kn = __ldcg(&A.key[nb]); gn = __ldcg(&A.gen[nb]); }
                     // mode 4: only neighbours across an inflow face of v matter
                     if (nb >= 0 && !(dm == 4 && !(sv & (1u << lane)))) {
                         if (sn & ST_RUNNING) d = drun = true;
@@ -2312,7 +2308,7 @@ k_async(CellArgs A)
                             if (dm == 5) d = gn < gv;
                             else if (dm == 2) d = kn < kv || (kn == kv && (uint32_t)nb < v);
                             else if (dm == 3) d = __uint_as_float(kn) + A.defer_delta < __uint_as_float(kv);
-                            else if (dm == 6 || dm == 9)   // strict total order (no deferral cycles)
+                            else if (dm == 6 || dm == 9)   // strict total order (no deferral cycles); mode 9: gen = level
                                 d = gn < gv || (gn == gv && (kn < kv || (kn == kv && (uint32_t)nb < v)));
                             else if (dm == 7)
                                 d = kn < kv || (kn == kv && (gn < gv || (gn == gv && (uint32_t)nb < v)));
@@ -2348,10 +2344,7 @@ k_async(CellArgs A)
                     continue;
                 }
                 got = v;
-                if (lane == 0) {   // (broadcast at the tags)
-                    gen_c = dm ? gv0 : (A.defer >= 5 ? __ldcg(&A.gen[v]) : 0u);
-                    gen2_c = gv20;   // (the level is kept in mode 9 only)
-                }
+                if (lane == 0) gen_c = dm ? gv0 : (A.defer >= 5 ? __ldcg(&A.gen[v]) : 0u);   // (broadcast at the tags)
                 break;
             }
             if (lane == 0) {
@@ -2392,7 +2385,6 @@ k_async(CellArgs A)
         if (!TAG1 && tid < 32) {
             tr_pid = __shfl_sync(0xffffffffu, tr_pid, 0);
             gen_c = __shfl_sync(0xffffffffu, gen_c, 0);
-            gen2_c = __shfl_sync(0xffffffffu, gen2_c, 0);
         }
         // TAG1: thread 0 hands what it holds in registers to warp 1 through S.plane / S.plane0
         // (free once the sweeps are over; five CTAs per SM leave no spare shared memory)
@@ -2400,7 +2392,6 @@ k_async(CellArgs A)
         if (TAG1 && tid == 0) {
             hand[0] = gen_c; hand[1] = tr_pid; hand[2] = tr_tag; hand[3] = tr_pop;
             reinterpret_cast<uint32_t*>(&S.plane0)[0] = tr_swept;
-            reinterpret_cast<uint32_t*>(&S.plane0)[1] = gen2_c;
         }
         __threadfence();   // value stores before the re-activations
         if constexpr (!TAG1) __syncthreads();
@@ -2464,14 +2455,14 @@ k_async(CellArgs A)
                     const int l = tid - 32;
                     const uint32_t cont = S.cont, dstate = S.dstate, cont_key = S.cont_key;
                     const unsigned long long st0 = S.stat[0], st1 = S.stat[1], st2 = S.stat[2];
-                    const uint32_t gen_w = hand[0], pid_w = hand[1], gen2_w = reinterpret_cast<uint32_t*>(&S.plane0)[1];
+                    const uint32_t gen_w = hand[0], pid_w = hand[1];
                     __syncwarp();
                     if (l == 0) S.stat[0] = S.stat[1] = S.stat[2] = 0;   // for the next processing
                     if (l < 6 && (S.face_flag & (1u << l))) {
                         const int64_t nc = face_neighbour(c, l, A.cps);
                         if (nc >= 0) {
                             atomicMin(&A.key[nc], tag_key<T, R>(A, S, l, nc));          // Eq. (3) / (4)
-                            if (A.defer == 9) atomicMin(&A.gen2[nc], gen2_w + 1u);
+                            if (A.defer == 9) atomicMin(&A.gen[nc], gen_w + 1u);   // (mode 9: the smallest level)
                             else if (A.defer >= 5) atomicMax(&A.gen[nc], gen_w + 1u);
                             if (A.trace) A.tagger[nc] = pid_w;
                             const uint32_t old = atomicOr(&A.state[nc], (1u << (l ^ 1)) | ST_QUEUED);
@@ -2497,7 +2488,7 @@ k_async(CellArgs A)
                 const int64_t nc = face_neighbour(c, tid, A.cps);
                 if (nc >= 0) {
                     atomicMin(&A.key[nc], tag_key<T, R>(A, S, tid, nc));          // Eq. (3) / (4)
-                    if (A.defer == 9) atomicMin(&A.gen2[nc], gen2_c + 1u);
+                    if (A.defer == 9) atomicMin(&A.gen[nc], gen_c + 1u);   // (mode 9: the smallest level)
                     else if (A.defer >= 5) atomicMax(&A.gen[nc], gen_c + 1u);
                     if (A.trace) A.tagger[nc] = tr_pid;
                     const uint32_t old = atomicOr(&A.state[nc], (1u << (tid ^ 1)) | ST_QUEUED);

@@ -659,6 +659,9 @@ template <int R> struct CellCfg {
 #ifndef EIK_DIR_VOTE
 #define EIK_DIR_VOTE 2   // sweep directions after the first from a vote of the active points (1: always, 2: when two or more axes are ambiguous)
 #endif
+#ifndef EIK_UNGATED_DIV
+#define EIK_UNGATED_DIV 32   // first sweep ungated from R^3 / 32 active points (measured 2 / 8 / 32 / 128 / always: C4 6.57 -> 6.42 ms at 32, others within 0.3 %; never ungated for face-activated cells: C3 +5 %)
+#endif
 #ifndef EIK_MINB16
 #define EIK_MINB16 5   // fp32 r = 16: 5 x 45.4 KB of shared memory, <= 64 registers (no spills)
 #endif
@@ -1870,7 +1873,7 @@ __device__ __forceinline__ void cell_process(const CellArgs& A, CellShared<R>& S
         ++nsweeps;
         uint32_t bwd = 0;
         {
-            const bool ungated = first && nact >= R3 / 8;
+            const bool ungated = first && nact >= R3 / EIK_UNGATED_DIV;
             if constexpr (R < EIK_DIR_TEMPLATE_MIN_R) {
                 bwd = sweep_dir<T, R, -1>(S, M, A.plane_tab, pm, ungated, nupd, nwr, nsteps, kap, dmax_, dir);
             } else if (R == 16 && EIK_SWEEP16 && kap == T(0)) {
